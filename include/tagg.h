@@ -1,0 +1,128 @@
+/*
+ * tagg.h -- C ABI of the B200-native padding-free FP8 grouped GEMM
+ * ("TMA-adaptive grouped GEMM", arxiv 2508.16584), libtagg.so.
+ *
+ * Plain pointers and sizes only: no torch types cross this boundary.  Every
+ * device pointer argument is a CUDA device address; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  All launches are
+ * stream-ordered and never synchronise the host.  Functions are reentrant.
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/tma_sim/):
+ *   tagg_grouped_gemm_fp8 -> engine.run_adaptive            engine.py:184-343
+ *   tagg_padded_baseline  -> engine.run_padded_baseline     engine.py:346-402
+ *     (implemented as tagg_pad_groups + tagg_grouped_gemm_fp8 + tagg_unpad_rows)
+ *   tagg_plan_group_stores-> descriptors.plan_group_stores  descriptors.py:117-129
+ *                            (+ plan_two_phase              descriptors.py:95-106)
+ *   tagg_pool_heights     -> descriptors.pool_heights       descriptors.py:31-35
+ *   tagg_pool_select      -> DescriptorPool.select          descriptors.py:48-54
+ *   tagg_plan_prefetch    -> prefetch.plan_prefetch         prefetch.py:50-72
+ *   tagg_validate_config  -> ProblemConfig.__post_init__    engine.py:77-92
+ *   tagg_pad_rows         -> workload.pad_rows              workload.py:59-65
+ * Error codes mirror the reference's exception hierarchy (errors.py:6-76).
+ */
+#ifndef TAGG_H
+#define TAGG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py) ---- */
+#define TAGG_OK 0
+#define TAGG_ERR_CONFIG (-1)            /* ConfigError          errors.py:14 */
+#define TAGG_ERR_INVALID_BLOCK_M (-2)   /* InvalidBlockM        errors.py:18 */
+#define TAGG_ERR_INVALID_BLOCK_N (-3)   /* InvalidBlockN        errors.py:22 */
+#define TAGG_ERR_SHAPE (-4)             /* ShapeMismatch        errors.py:71 */
+#define TAGG_ERR_ALIGNMENT (-5)         /* AlignmentError       errors.py:30-40 */
+#define TAGG_ERR_NO_ALIGNED_SOLUTION (-6) /* NoAlignedSolution  errors.py:64-68 */
+#define TAGG_ERR_RES_OUT_OF_RANGE (-7)  /* ResOutOfRange        errors.py:60 */
+#define TAGG_ERR_UNSUPPORTED (-8)       /* shape exceeds this build's on-chip budget */
+#define TAGG_ERR_CUDA (-9)              /* CUDA runtime / driver failure */
+
+/* ---- B operand storage ---- */
+#define TAGG_B_KN 0 /* [G_b, K, N], N contiguous (reference layout, engine.py:137) */
+#define TAGG_B_NK 1 /* [G_b, N, K], K contiguous (transposed weights, dgrad)      */
+
+/* ---- flags ---- */
+#define TAGG_FLAG_EXACT_PROMOTION 1u /* s=fl(sa*sb); acc=fl(acc+fl(inner*s)) with two roundings
+                                        (engine.py:161-164) instead of one FFMA2 */
+#define TAGG_FLAG_PLAIN_C_STAGING 2u /* unswizzled C staging + SWIZZLE_NONE store pool */
+
+#define TAGG_TILE_MAP_FIELDS 9
+
+/*
+ * Padding-free grouped GEMM: for every group g with M_g rows (rows stacked
+ * along M in A, group g starting at sum(M_0..M_{g-1})):
+ *   C[c_row0(g) + i, n] = bf16( sum_kb  inner_kb(i, n) * fl(SA[row, kb] * SB_g[kb, n/128]) )
+ * with inner_kb the exact-product FP8 dot product over the 128-wide k block
+ * (tensor cores) and the k-block sum accumulated in fp32 registers in
+ * ascending kb (engine.py:294-314).
+ *
+ *  a              [m_alloc, K] e4m3fn codes, row stride lda bytes (lda % 16 == 0)
+ *  sa             [m_alloc, ceil(K/128)] fp32, K-major, dense (row stride 4*ceil(K/128) B)
+ *  b              b_layout TAGG_B_KN: [b_experts, K, N]; TAGG_B_NK: [b_experts, N, K];
+ *                 b_experts == 1 shares one B across all groups (reference API)
+ *  sb             fp32 scales; element (g, kb, nb) at sb[g*sb_stride_g + kb*sb_stride_kb +
+ *                 nb*sb_stride_nb] (strides in floats; sb_stride_g = 0 for a shared B)
+ *  group_sizes    DEVICE int32 [G], M_g >= 0, sum <= m_alloc (not read by the host)
+ *  c              [c_rows, N] bf16 bits, row stride ldc elements (ldc % 8 == 0)
+ *  c_row_offsets  nullable DEVICE int64 [G]: output row of group g's first row;
+ *                 NULL = contiguous (same rows as A)
+ *  tile_map       nullable DEVICE int32 [tagg_max_tiles(), 9]: per tile
+ *                 (g, m_tile, n0, a_row0, valid, d, phaseA_row, phaseB_smem_row, phaseB_row),
+ *                 the exact store geometry the kernel used; unused rows untouched
+ *  flags          TAGG_FLAG_*
+ *
+ * Only C rows [c_row0(g), c_row0(g) + M_g) of each group are written.  No row
+ * beyond M_g is ever stored: residual tiles use the power-of-two TMA
+ * descriptor pool with the dual-phase store (descriptors.py:95-106).
+ */
+int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa, int64_t m_alloc,
+                          const void* b, int b_layout, int b_experts, const float* sb,
+                          int64_t sb_stride_g, int64_t sb_stride_kb, int64_t sb_stride_nb,
+                          const int32_t* group_sizes, int G, int N, int K, void* c, int64_t ldc,
+                          int64_t c_rows, const int64_t* c_row_offsets, int32_t* tile_map,
+                          uint32_t flags, void* stream);
+
+/* Upper bound on the tile count, to size tile_map (no device data needed). */
+int64_t tagg_max_tiles(int64_t m_alloc, int G, int N);
+
+/*
+ * Baseline K2 (engine.py:369-373): copy each group into a 128-row-aligned
+ * slot, A pad rows = 0, S_A pad rows = 1.0.  a_pad / sa_pad need
+ * tagg_padded_rows_bound(m_alloc, G) rows.  padded_sizes (DEVICE int32 [G])
+ * receives ceil(M_g/128)*128.
+ */
+int tagg_pad_groups(const void* a, int64_t lda, const float* sa, const int32_t* group_sizes, int G,
+                    int K, void* a_pad, float* sa_pad, int32_t* padded_sizes, int64_t m_pad_alloc,
+                    void* stream);
+/* Baseline K3 (engine.py:399-401): gather each group's valid rows from C_pad. */
+int tagg_unpad_rows(const void* c_pad, const int32_t* group_sizes, int G, int N, void* c,
+                    int64_t m_alloc, void* stream);
+int64_t tagg_padded_rows_bound(int64_t m_alloc, int G);
+
+/* ---- host planners (no GPU needed) ---- */
+/* ProblemConfig validation (engine.py:77-92). */
+int tagg_validate_config(int64_t n, int64_t k, const int64_t* group_sizes, int G, int64_t block_m,
+                         int64_t block_n, int64_t block_k);
+/* Per group 8 int64: group, rows, full_tiles, res, desc, a_smem, a_gmem, b_smem, b_gmem
+   (res = 0 and the phase fields = -1 when the group divides evenly).  out: [G, 9]. */
+int tagg_plan_group_stores(const int64_t* group_sizes, int G, int64_t block_rows, int64_t* out);
+/* Pool heights 1..block_rows (powers of two); returns the count or an error. */
+int tagg_pool_heights(int64_t block_rows, int64_t* out, int cap);
+/* Largest pool height <= residual_rows; TAGG_ERR_RES_OUT_OF_RANGE outside [1, block_rows]. */
+int64_t tagg_pool_select(int64_t residual_rows, int64_t block_rows);
+/* out[4] = start_addr, row_prev, row_next, total_rows. */
+int tagg_plan_prefetch(int64_t tile_start_addr, int64_t row_bytes, int64_t block_rows, int64_t* out);
+int64_t tagg_pad_rows(const int64_t* group_sizes, int G, int64_t block_rows);
+
+const char* tagg_error_string(int code);
+int tagg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAGG_H */

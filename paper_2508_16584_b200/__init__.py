@@ -1,0 +1,52 @@
+"""B200-native padding-free FP8 grouped GEMM (arxiv 2508.16584).
+
+The hot path is one hand-written sm_100a kernel (csrc/tagg_gemm.cu) behind the
+C ABI in include/tagg.h.  This package is the host-side mirror of the
+reference's Python entry points (tma_sim.engine / descriptors / prefetch /
+workload), with the same names, argument meanings and exceptions.
+"""
+
+from .engine import (  # noqa: F401
+    AdaptiveRun,
+    BitwiseReport,
+    GroupedOperands,
+    PaddedWorkspace,
+    ProblemConfig,
+    bf16_from_f32,
+    f32_from_bf16,
+    grouped_gemm_fp8,
+    max_tiles,
+    pad_groups,
+    padded_grouped_gemm_fp8,
+    run_adaptive,
+    run_padded_baseline,
+    unpad_rows,
+    verify_bitwise,
+)
+from .errors import (  # noqa: F401
+    AlignmentError,
+    ConfigError,
+    CudaError,
+    InvalidBlockM,
+    InvalidBlockN,
+    NoAlignedSolution,
+    ResOutOfRange,
+    ShapeMismatch,
+    SimError,
+    Unsupported,
+)
+from .planning import (  # noqa: F401
+    account,
+    build_pool,
+    format_plan,
+    generate_group_sizes,
+    pad_rows,
+    plan_group_stores,
+    plan_prefetch,
+    plan_two_phase,
+    pool_heights,
+    scale_row_bytes,
+    window_rows,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,225 @@
+"""GPU parity: the sm_100a kernel (through the C ABI) against the CPU oracle.
+
+Every comparison uses the oracle (oracle/, pinned to the reference's own
+goldens in test_oracle.py), the committed golden fixtures, or a
+size-independent property.  Values must lie within helpers.REL_TOL.  The
+index map and the untouched-memory checks are bit-exact.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from helpers import assert_parity, oracle_c, per_expert_operands, tolerance_report  # noqa: E402
+from oracle import fp8 as ofp8  # noqa: E402
+from oracle import plan as oplan  # noqa: E402
+from tmas import CASES, load_case  # noqa: E402
+
+import paper_2508_16584_b200 as tg  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _cfg_ops(case):
+    layout = "nk" if case.get("b_layout") == "expert_nk" else "kn"
+    cfg = tg.ProblemConfig(n=case["n"], k=case["k"], group_sizes=tuple(case["group_sizes"]))
+    ops = tg.GroupedOperands(case["a_codes"], case["a_scales"], case["b_codes"], case["b_scales"], b_layout=layout)
+    return cfg, ops, layout
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("mode", ["ffma2", "exact", "plain_staging"])
+def test_golden_fixtures(name, mode):
+    case = load_case(name)
+    cfg, ops, _ = _cfg_ops(case)
+    run = tg.run_adaptive(cfg, ops, exact_promotion=(mode == "exact"), plain_staging=(mode == "plain_staging"))
+    rep = assert_parity(run.c_bits, case["c_golden"], label=f"{name}/{mode}")
+    print(f"{name}/{mode}: {rep}")
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_tile_map_is_bit_exact(name):
+    """The store geometry the kernel used equals the reference tile loop (engine.py:269-335)."""
+    case = load_case(name)
+    cfg, ops, _ = _cfg_ops(case)
+    run = tg.run_adaptive(cfg, ops)
+    got = sorted(tuple(int(x) for x in r) for r in run.tile_map)
+    want = sorted(oplan.tile_map(cfg.group_sizes, cfg.n))
+    assert got == want
+
+
+@pytest.mark.parametrize("name", ["c1", "k640", "perexpert"])
+def test_padded_baseline_equals_adaptive_bitwise(name):
+    """Paper claim: the padding-free path is bitwise identical to
+    pad + padded GEMM on the valid rows."""
+    case = load_case(name)
+    cfg, ops, _ = _cfg_ops(case)
+    a = tg.run_adaptive(cfg, ops).c_bits
+    b = tg.run_padded_baseline(cfg, ops)
+    assert tg.verify_bitwise(a, b).equal
+
+
+def test_poison_never_reaches_output_and_all_rows_written():
+    case = load_case("k640")
+    cfg, ops, _ = _cfg_ops(case)
+    outs = [tg.run_adaptive(cfg, ops, poison=p).c_bits for p in (0xA5, 0x5A, 0x7F)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def _dev(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+    return t if dtype is None else t.to(dtype)
+
+
+@pytest.mark.parametrize("gap", [1, 3, 128])
+def test_untouched_memory_between_groups(gap):
+    """No row beyond M_g is ever written: sentinel rows between groups survive."""
+    sizes = (1, 67, 128, 255, 0, 129, 200, 64, 3)
+    n, k = 192, 384
+    ac, asc, bc, bsc = per_expert_operands(sizes, n, k, 21)
+    offs, o = [], 0
+    for s in sizes:
+        offs.append(o)
+        o += s + gap
+    sentinel = 0x7BCD
+    out = torch.full((o, n), sentinel, dtype=torch.int16, device=DEV)
+    tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
+                        out=out, c_row_offsets=_dev(np.array(offs, np.int64)))
+    got = out.cpu().numpy().view(np.uint16)
+    want = oracle_c(ac, asc, bc, bsc, sizes)
+    a = 0
+    for g, s in enumerate(sizes):
+        assert_parity(got[offs[g]:offs[g] + s], want[a:a + s], label=f"group {g}")
+        assert np.all(got[offs[g] + s:offs[g] + s + gap] == sentinel), f"gap after group {g} written"
+        a += s
+
+
+def test_residual_sweep_every_residue_small():
+    """Every M_g mod 128 in 1..127 (configs[1] pattern, M_g = 128*g + r) at N=128, K=256."""
+    n, k = 128, 256
+    for r0 in range(1, 128, 16):
+        sizes = tuple(128 * g + ((r0 + g) % 127 + 1) for g in range(8))
+        ac, asc, bc, bsc = per_expert_operands(sizes, n, k, r0)
+        cfg = tg.ProblemConfig(n=n, k=k, group_sizes=sizes)
+        run = tg.run_adaptive(cfg, tg.GroupedOperands(ac, asc, bc, bsc))
+        assert_parity(run.c_bits, oracle_c(ac, asc, bc, bsc, sizes), label=f"r0={r0}")
+        got = sorted(tuple(int(x) for x in rr) for rr in run.tile_map)
+        assert got == sorted(oplan.tile_map(sizes, n))
+
+
+def _synthetic(sizes, n, k, seed, layout="kn"):
+    """Fast synthetic operands (uniform finite e4m3 codes, positive fp32 scales)."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    m = int(sum(sizes))
+    G = len(sizes)
+    kb, nb = -(-k // 128), -(-n // 128)
+
+    def codes(*shape):
+        c = torch.randint(0, 256, shape, generator=g, dtype=torch.int32)
+        c = torch.where((c & 0x7F) == 0x7F, c - 1, c)  # avoid the two NaN codes
+        return c.to(torch.uint8).numpy()
+
+    def scales(*shape):
+        e = torch.randint(-12, -4, shape, generator=g).float()
+        return (torch.rand(shape, generator=g) * 0.5 + 0.5).mul(torch.exp2(e)).numpy().astype(np.float32)
+
+    ac, asc = codes(m, k), scales(m, kb)
+    if layout == "kn":
+        bc, bsc = codes(G, k, n), scales(G, kb, nb)
+    else:
+        bc, bsc = codes(G, n, k), scales(G, nb, kb)
+    return ac, asc, bc, bsc
+
+
+@pytest.mark.parametrize("layout", ["kn", "nk"])
+def test_deepseek_shape_sampled_columns(layout):
+    """DeepSeek-V3 gate+up shape (N=4096, K=7168) with ragged groups.  Parity is
+    checked on two 128-column slices and all rows against the oracle."""
+    sizes = (300, 0, 1, 1024, 77, 513, 128, 255)
+    n, k = 4096, 7168
+    ac, asc, bc, bsc = _synthetic(sizes, n, k, 7, layout)
+    out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
+                              b_layout=layout)
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    for n0 in (0, 2944):
+        want = np.zeros((sum(sizes), n), dtype=np.uint16)
+        oracle_c(ac, asc, bc, bsc, sizes, b_layout=layout, n_range=(n0, n0 + 128), out=want)
+        rep = assert_parity(got[:, n0:n0 + 128], want[:, n0:n0 + 128], label=f"n0={n0}")
+        print(f"deepseek {layout} n0={n0}: {rep}")
+
+
+def test_k_tail_and_n_tail_shapes():
+    sizes = (5, 130, 37)
+    for n, k in ((64, 16), (192, 208), (320, 1664), (64, 4112)):
+        ac, asc, bc, bsc = _synthetic(sizes, n, k, n + k)
+        out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)))
+        got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+        assert_parity(got, oracle_c(ac, asc, bc, bsc, sizes), label=f"n={n} k={k}")
+
+
+def test_shared_b_reference_api_and_empty_groups():
+    sizes = (0, 0, 131, 0)
+    n, k = 256, 512
+    ac, asc, bc, bsc = ofp8.random_operands(sum(sizes), n, k, 4)
+    run = tg.run_adaptive(tg.ProblemConfig(n=n, k=k, group_sizes=sizes), tg.GroupedOperands(ac, asc, bc, bsc))
+    assert_parity(run.c_bits, oracle_c(ac, asc, bc, bsc, sizes))
+    empty = tg.run_adaptive(tg.ProblemConfig(n=64, k=64, group_sizes=(0,)),
+                            tg.GroupedOperands(np.zeros((0, 64), np.uint8), np.zeros((0, 1), np.float32),
+                                               np.zeros((64, 64), np.uint8), np.ones((1, 1), np.float32)))
+    assert empty.c_bits.shape == (0, 64)
+
+
+def test_device_group_sizes_without_host_sync_under_graph_capture():
+    """The whole call is capturable in a CUDA graph.  Group sizes live on the
+    device and can change between replays."""
+    sizes = [100, 200, 50]
+    n, k = 256, 256
+    ac, asc, bc, bsc = _synthetic((512, 0, 0), n, k, 3)  # 512 rows, 3 experts
+    a, sa, b, sb = _dev(ac), _dev(asc), _dev(bc), _dev(bsc)
+    gs = _dev(np.array(sizes, np.int32))
+    out = torch.zeros((512, n), dtype=torch.bfloat16, device=DEV)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        tg.grouped_gemm_fp8(a, sa, b, sb, gs, out=out)  # warm-up (sets smem attribute)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        tg.grouped_gemm_fp8(a, sa, b, sb, gs, out=out)
+    for new in ([100, 200, 50], [1, 127, 384], [0, 512, 0]):
+        gs.copy_(torch.tensor(new, dtype=torch.int32))
+        out.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+        m = sum(new)
+        assert_parity(got[:m], oracle_c(ac[:m], asc[:m], bc, bsc, new), label=str(new))
+        assert np.all(got[m:] == 0)
+
+
+def test_error_mapping():
+    a = torch.zeros((4, 128), dtype=torch.uint8, device=DEV)
+    sa = torch.ones((4, 1), dtype=torch.float32, device=DEV)
+    b = torch.zeros((128, 96), dtype=torch.uint8, device=DEV)
+    sb = torch.ones((1, 1), dtype=torch.float32, device=DEV)
+    gs = torch.tensor([4], dtype=torch.int32, device=DEV)
+    with pytest.raises(tg.ConfigError):
+        tg.grouped_gemm_fp8(a, sa, b, sb, gs)  # N = 96 is not a multiple of 64
+    b = torch.zeros((130, 128), dtype=torch.uint8, device=DEV)
+    with pytest.raises(tg.ShapeMismatch):
+        tg.grouped_gemm_fp8(a, sa, b, sb, gs)
+
+
+def test_identical_fraction_reported_for_reference_recipe():
+    """The reference input recipe at configs[0]: report the bit-identical fraction."""
+    case = load_case("c1")
+    cfg, ops, _ = _cfg_ops(case)
+    for exact in (False, True):
+        run = tg.run_adaptive(cfg, ops, exact_promotion=exact)
+        rep = tolerance_report(run.c_bits, case["c_golden"])
+        print(f"c1 exact={exact}: {rep}")
+        assert rep["out_of_tol"] == 0
+        assert rep["bit_identical"] > 0.9
