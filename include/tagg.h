@@ -50,6 +50,12 @@ extern "C" {
 #define TAGG_FLAG_EXACT_PROMOTION 1u /* s=fl(sa*sb); acc=fl(acc+fl(inner*s)) with two roundings
                                         (engine.py:161-164) instead of one FFMA2 */
 #define TAGG_FLAG_PLAIN_C_STAGING 2u /* unswizzled C staging + SWIZZLE_NONE store pool */
+#define TAGG_FLAG_SINGLE_CTA 4u      /* 128x128 tiles on one CTA (tcgen05 cta_group::1) instead of the
+                                        default CTA-pair tile (cta_group::2) */
+#define TAGG_FLAG_TILE_N128 8u       /* CTA-pair tile 256x128 (more, smaller tiles: fewer idle SMs
+                                        in the last wave of small problems) */
+#define TAGG_FLAG_TILE_N256 16u      /* CTA-pair tile 256x256 (half the operand traffic per FLOP);
+                                        without either flag the launcher picks by wave efficiency */
 
 #define TAGG_TILE_MAP_FIELDS 9
 

@@ -6,21 +6,30 @@
 //     for kb ascending: acc = acc + inner_kb(i, n) * fl(SA[row, kb] * SB_g[kb, n / 128])
 //     C[c_row0(g) + i, n] = bf16_rne(acc)
 //
-// One persistent CTA per SM walks a static tile schedule.  The tile -> group
-// map comes from a prefix sum over the DEVICE group sizes, computed in each
-// CTA's prologue with no host sync.  Warp roles:
+// Persistent kernel; a static tile schedule over the DEVICE group sizes (a
+// warp prefix sum in every CTA's prologue, no host sync).  Two tile shapes
+// share one template:
+//   kCG = 2 (default): a CTA pair (cluster of 2, tcgen05 cta_group::2) owns a
+//       256 x 256 output tile.  Each CTA holds 128 rows x 256 columns of fp32
+//       partials in TMEM (2 buffers x 256 columns) and stages its own 128 rows
+//       of A and its 128-column half of B.  Per-SM smem and L2 traffic per
+//       FLOP is half that of a 128 x 128 tile.
+//   kCG = 1: one CTA owns a 128 x 128 tile (4 TMEM buffers x 128 columns).
+// Warp roles (per CTA, 384 threads = 3 warpgroups; setmaxnreg moves registers
+// from warpgroup 0 to the promotion warpgroups):
 //   warp 0 : TMA producer.  A [128 x 128] and B [128 x 128] boxes go into
 //            128B-swizzled smem (S-stage mbarrier ring).  The tile's S_A rows
 //            arrive by one over-fetching 1-D bulk copy whose start slides back
 //            row_prev rows onto a 16-byte boundary (prefetch.py:50-72).
-//   warp 1 : TMEM allocator + single-thread tcgen05.mma issuer.  Per 128-K
-//            block it issues 4 x kind::f8f6f4 (M=128, N=128, K=32) into a fresh
-//            TMEM accumulator (4 buffers x 128 columns = all 512 columns).
-//   warps 2-9 : promotion + epilogue.  Each thread owns one row and 64
+//   warp 1 : TMEM allocator.  In the leader CTA it is also the MMA issuer: per
+//            128-K block, 4 x tcgen05.mma kind::f8f6f4 (K=32) into a fresh TMEM
+//            accumulator.
+//   warp 2 : the group-table prefix sums in the prologue.
+//   warps 4-11 : promotion + epilogue.  Each thread owns one row and BN/2
 //            columns.  Per k-block it does tcgen05.ld of the partial,
 //            s = fl(sa * sb), acc += partial * s in fp32 registers (FFMA2, or
 //            FMUL+FADD with TAGG_FLAG_EXACT_PROMOTION), ascending kb.  At tile
-//            end: bf16 -> swizzled smem staging -> TMA store.  Full tiles use
+//            end: bf16 -> swizzled smem staging -> TMA stores.  Full tiles use
 //            the 128-row descriptor.  Residual tiles pick d = 2^floor(log2 res)
 //            from the 8-entry store pool and issue the dual-phase store
 //            (descriptors.py:95-106), so no row past M_g is ever written.
@@ -39,17 +48,25 @@
 
 namespace tagg {
 
-constexpr int BM = 128, BN = 128, BK = 128;
-constexpr int kNumAcc = 4;  // TMEM accumulation buffers of BN columns
+constexpr int BM = 128, BK = 128;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kNumPromoWarps = 8;
-constexpr int kThreads = 64 + 32 * kNumPromoWarps;
+constexpr int kFirstPromoWarp = 4;  // warpgroup 0: producer, MMA, table scan, spare
+constexpr int kThreads = 32 * (kFirstPromoWarp + kNumPromoWarps);
+// setmaxnreg budgets.  The CTA owns 168 x 384 = 64512 registers (ptxas' launch
+// allocation), so 128 * kRegsControl + 256 * kRegsPromo must not exceed 64512, or
+// the promotion warpgroups' setmaxnreg.inc never completes.
+constexpr uint32_t kRegsLaunch = 168;
+constexpr uint32_t kRegsControl = 72;
+constexpr uint32_t kRegsPromo = 216;
+static_assert(128 * kRegsControl + 256 * kRegsPromo <= 384 * kRegsLaunch, "setmaxnreg budget exceeds the CTA pool");
 constexpr int kMaxStages = 8;
-constexpr uint32_t kStageBytesA = BM * BK;
-constexpr uint32_t kStageBytesB = BK * BN;
+constexpr uint32_t kStageBytesA = BM * BK;   // 128 rows x 128 K
 constexpr uint32_t kChunkBytesC = BM * 128;  // 128 rows x 64 bf16 columns
 constexpr uint32_t kCStagingBytes = 2 * kChunkBytesC;
 constexpr int kPoolSize = 8;  // heights 1, 2, ..., 128 (descriptors.py:31-35)
+constexpr uint32_t kDbgNoLoad = 1u << 8;     // diagnostics: producer signals stages without loads
+constexpr uint32_t kDbgNoPromote = 1u << 9;  // diagnostics: promotion skips tcgen05.ld + math
 
 struct Params {
   CUtensorMap tmap_a;
@@ -65,13 +82,30 @@ struct Params {
   int32_t G, N, K, kb_count, n_tiles, sa_rb, b_kmajor, b_shared;
   uint32_t stages, sa_buf_bytes;
   uint32_t off_a, off_b, off_c, off_sa, off_tab, off_bar;
+  uint32_t dbg;
+};
+
+template <int kCG, int kBN_>
+struct Cfg {
+  static constexpr int kBN = kBN_;                   // output columns per (pair) tile = MMA N
+  static constexpr int kTileM = BM * kCG;            // rows per scheduled (pair) tile = MMA M
+  static constexpr int kBCols = kBN / kCG;           // B columns staged by each CTA
+  static constexpr uint32_t kStageBytesB = BK * kBCols;
+  static constexpr int kNumAcc = 512 / kBN;          // TMEM accumulation buffers
+  static constexpr int kColsPerThread = kBN / 2;     // two warps per TMEM lane quarter
+  static constexpr uint32_t kStageTx = kCG * (kStageBytesA + kStageBytesB);  // bytes landing per stage
+  static_assert(kBCols == 64 || kBCols == 128, "B share per CTA must be 64 or 128 columns");
 };
 
 struct Tile {
   int g, mt, n0, row0, valid, crow0;
 };
 
-__device__ __forceinline__ Tile decode_tile(int t, const int32_t* tab_tile, const int32_t* tab_row,
+// Scheduled tile t -> this CTA's 128-row slice.  A scheduled tile covers
+// kTileM rows (pair index pm) x kBN columns of group g; CTA `rank` owns rows
+// [pm*kTileM + 128*rank, +128).  valid <= 0 when the slice lies past M_g.
+template <int kCG, int kBN>
+__device__ __forceinline__ Tile decode_tile(int t, int rank, const int32_t* tab_tile, const int32_t* tab_row,
                                             const int32_t* tab_size, const int32_t* tab_crow, int G) {
   int lo = 0, hi = G - 1;  // largest g with tab_tile[g] <= t
   while (lo < hi) {
@@ -82,9 +116,17 @@ __device__ __forceinline__ Tile decode_tile(int t, const int32_t* tab_tile, cons
   T.g = lo;
   const int l = t - tab_tile[lo];
   const int m = tab_size[lo];
-  const int mtiles = (m + BM - 1) / BM;
-  T.mt = l % mtiles;
-  T.n0 = (l / mtiles) * BN;
+  const int ptiles = (m + Cfg<kCG, kBN>::kTileM - 1) / Cfg<kCG, kBN>::kTileM;
+  const int ntiles = (tab_tile[lo + 1] - tab_tile[lo]) / ptiles;
+  // Grouped raster: super-rows of kRasterM (pair-)m-tiles, n-tiles outer, so the
+  // ~74-148 concurrently active tiles share a few A row blocks and B column blocks in L2.
+  constexpr int kRasterM = 8;
+  const int sr = l / (kRasterM * ntiles);
+  const int h = min(kRasterM, ptiles - sr * kRasterM);
+  const int local = l - sr * kRasterM * ntiles;
+  const int pm = sr * kRasterM + local % h;
+  T.mt = pm * kCG + rank;
+  T.n0 = (local / h) * Cfg<kCG, kBN>::kBN;
   T.row0 = tab_row[lo] + T.mt * BM;
   T.valid = min(BM, m - T.mt * BM);
   T.crow0 = tab_crow[lo] + T.mt * BM;
@@ -100,14 +142,19 @@ __device__ __forceinline__ int sa_row_prev(int64_t row0, int rb) {
   return rp;
 }
 
-template <bool kExact, bool kSwizzleC>
+template <int kCG, int kBN, bool kExact, bool kSwizzleC>
 __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_constant__ Params p) {
+  using C = Cfg<kCG, kBN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t S = p.stages;
   const int G = p.G;
+  const int rank = (kCG == 2) ? static_cast<int>(cluster_ctarank()) : 0;
+  const bool is_leader = rank == 0;
+  const int cluster_id = blockIdx.x / kCG;
+  const int num_clusters = gridDim.x / kCG;
 
   uint8_t* sA = smem + p.off_a;
   uint8_t* sB = smem + p.off_b;
@@ -121,8 +168,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
-  uint64_t* tempty = tfull + kNumAcc;
-  uint64_t* safull = tempty + kNumAcc;
+  uint64_t* tempty = tfull + C::kNumAcc;
+  uint64_t* safull = tempty + C::kNumAcc;
   uint64_t* saempty = safull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(saempty + 2);
 
@@ -131,12 +178,12 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     prefetch_tmap(&p.tmap_a);
     prefetch_tmap(&p.tmap_b);
     for (uint32_t i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&full[i], 1);   // the leader's arrive.expect_tx; TMA bytes of both CTAs
+      mbar_init(&empty[i], 1);  // the MMA commit (multicast to both CTAs)
     }
-    for (int i = 0; i < kNumAcc; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kNumPromoWarps);
+    for (int i = 0; i < C::kNumAcc; ++i) {
+      mbar_init(&tfull[i], 1);                         // MMA commit
+      mbar_init(&tempty[i], kNumPromoWarps * kCG);     // promotion warps of every CTA in the pair
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&safull[i], 1);
@@ -144,14 +191,14 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 1) tmem_alloc<kCG>(tmem_slot, kTmemCols);
   if (warp == 2) {
-    // device-side prefix sums over M_g: row offsets and tile offsets
+    // device-side prefix sums over M_g: row offsets and (pair-)tile offsets
     int carry_r = 0, carry_t = 0;
     for (int base = 0; base < G; base += 32) {
       const int g = base + lane;
       const int m = (g < G) ? max(0, p.group_sizes[g]) : 0;
-      const int tl = ((m + BM - 1) / BM) * p.n_tiles;
+      const int tl = ((m + C::kTileM - 1) / C::kTileM) * p.n_tiles;
       int im = m, it = tl;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -174,22 +221,25 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = tab_tile[G];
   const int kbc = p.kb_count;
   const int rb = p.sa_rb;
 
-  if (warp == 0) {
+  if (warp < kFirstPromoWarp) {
+   setmaxnreg_dec<kRegsControl>();
+   if (warp == 0) {
     // ========================================================== TMA producer
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0, sab = 0, saph = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const Tile T = decode_tile(t, tab_tile, tab_row, tab_size, tab_crow, G);
-        const int gb = p.b_shared ? 0 : T.g;
-        // ---- S_A over-fetch window (one 1-D bulk copy per tile)
-        mbar_wait(&saempty[sab], saph ^ 1);
+    uint32_t stage = 0, phase = 0, sab = 0, saph = 0;
+    const bool elected = elect_one();
+    for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+      const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
+      const int gb = p.b_shared ? 0 : T.g;
+      // ---- S_A over-fetch window (one 1-D bulk copy per tile, own rows)
+      mbar_wait(&saempty[sab], saph ^ 1);
+      if (elected) {
         const int rp = sa_row_prev(T.row0, rb);
         const int64_t start_row = static_cast<int64_t>(T.row0) - rp;
         const int64_t want = ((static_cast<int64_t>(rp + BM) * rb) + 15) & ~int64_t(15);
@@ -204,67 +254,100 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           *reinterpret_cast<float*>(dst + bulk + i) = __ldg(reinterpret_cast<const float*>(src + bulk + i));
         mbar_arrive_expect_tx(&safull[sab], bulk);
         if (bulk) bulk_load_1d(dst, src, bulk, &safull[sab]);
-        if (++sab == 2) { sab = 0; saph ^= 1; }
-        // ---- A / B k-blocks
-        for (int kb = 0; kb < kbc; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], kStageBytesA + kStageBytesB);
-          tma_load_2d(&p.tmap_a, &full[stage], sA + stage * kStageBytesA, kb * BK, T.row0);
-          if (p.b_kmajor)
-            tma_load_3d(&p.tmap_b, &full[stage], sB + stage * kStageBytesB, kb * BK, T.n0, gb);
-          else
-            tma_load_3d(&p.tmap_b, &full[stage], sB + stage * kStageBytesB, T.n0, kb * BK, gb);
-          if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+      __syncwarp();
+      if (++sab == 2) { sab = 0; saph ^= 1; }
+      // ---- A / B k-blocks.  This CTA stages its 128 rows of A and its
+      // 128-column share of B; completion is counted on the leader's barrier.
+      const int nb = T.n0 + rank * C::kBCols;
+      for (int kb = 0; kb < kbc; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elected) {
+          if (p.dbg & kDbgNoLoad) {
+            if (is_leader) mbar_arrive(&full[stage]);
+          } else {
+            if (is_leader) mbar_arrive_expect_tx(&full[stage], C::kStageTx);
+            const int cb0 = p.b_kmajor ? kb * BK : nb;
+            const int cb1 = p.b_kmajor ? nb : kb * BK;
+            if constexpr (kCG == 1) {
+              tma_load_2d(&p.tmap_a, &full[stage], sA + stage * kStageBytesA, kb * BK, T.row0);
+              tma_load_3d(&p.tmap_b, &full[stage], sB + stage * C::kStageBytesB, cb0, cb1, gb);
+            } else {
+              tma_load_2d_cg2(&p.tmap_a, &full[stage], sA + stage * kStageBytesA, kb * BK, T.row0);
+              tma_load_3d_cg2(&p.tmap_b, &full[stage], sB + stage * C::kStageBytesB, cb0, cb1, gb);
+            }
+          }
         }
+        __syncwarp();
+        if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
+    // Producer tail: wait until every issued stage has been consumed, so no MMA
+    // commit can still target this CTA's barriers after it exits.
+    for (uint32_t i = 0; i < S; ++i) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      if (++stage == S) { stage = 0; phase ^= 1; }
+    }
   } else if (warp == 1) {
-    // ========================================================== MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = idesc_e4m3_f32(BM, BN, p.b_kmajor == 0);
+    // ========================================================== MMA issuer (leader CTA)
+    if (is_leader) {
+      const uint32_t idesc = idesc_e4m3_f32(BM * kCG, C::kBN, p.b_kmajor == 0);
+      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), 16, 1024);
+      // B: K-major rows are 128 B (SWIZZLE_128B, 8-row groups of 1 KB).  MN-major rows
+      // hold this CTA's kBCols columns: 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B,
+      // 8-row groups of 512 B).  The descriptor advances by 32 K per MMA.
+      const uint64_t b_desc0 =
+          p.b_kmajor ? umma_desc_sw128(smem_u32(sB), 16, 1024)
+                     : (C::kBCols == 128 ? umma_desc_sw128(smem_u32(sB), C::kStageBytesB, 1024)
+                                         : umma_desc_sw64(smem_u32(sB), C::kStageBytesB, 512));
+      const uint32_t b_kstep = p.b_kmajor ? (32u >> 4) : ((32u * C::kBCols) >> 4);  // desc units per K=32
+      const bool elected = elect_one();
       uint32_t stage = 0, phase = 0, acc = 0, accph = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         for (int kb = 0; kb < kbc; ++kb) {
           mbar_wait(&tempty[acc], accph ^ 1);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * kStageBytesA);
-          const uint32_t b_base = smem_u32(sB + stage * kStageBytesB);
-          const uint32_t d_tmem = tmem_base + acc * BN;
+          if (elected) {
+            const uint64_t ad = a_desc0 + ((stage * kStageBytesA) >> 4);
+            const uint64_t bd = b_desc0 + ((stage * C::kStageBytesB) >> 4);
+            const uint32_t d_tmem = tmem_base + acc * C::kBN;
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k) {
-            const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bd = p.b_kmajor ? umma_desc_sw128(b_base + k * 32, 16, 1024)
-                                           : umma_desc_sw128(b_base + k * 32 * BN, kStageBytesB, 1024);
-            mma_f8f6f4(d_tmem, ad, bd, idesc, k > 0 ? 1u : 0u);
+            for (int k = 0; k < BK / 32; ++k)
+              mma_f8f6f4<kCG>(d_tmem, ad + static_cast<uint64_t>(k * (32 >> 4)),
+                              bd + static_cast<uint64_t>(k * b_kstep), idesc, k > 0 ? 1u : 0u);
+            mma_commit<kCG>(&empty[stage]);  // smem slot free (both CTAs) once these MMAs retire
+            mma_commit<kCG>(&tfull[acc]);    // k-block partial ready for promotion (both CTAs)
           }
-          mma_commit(&empty[stage]);  // smem slot free once these MMAs retire
-          mma_commit(&tfull[acc]);    // k-block partial ready for promotion
+          __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
-          if (++acc == kNumAcc) { acc = 0; accph ^= 1; }
+          if (++acc == C::kNumAcc) { acc = 0; accph ^= 1; }
         }
       }
     }
+   }
   } else {
+    setmaxnreg_inc<kRegsPromo>();
     // ========================================================== promotion + epilogue
-    const int pw = warp - 2;
+    constexpr int kCPT = C::kColsPerThread;  // 64 or 128
+    const int pw = warp - kFirstPromoWarp;
     const int q = warp & 3;          // TMEM lane quarter this warp may access
-    const int half = pw >> 2;        // column half [64*half, 64*half + 64)
+    const int half = pw >> 2;        // column half [kCPT*half, kCPT*half + kCPT)
     const int r = 32 * q + lane;     // tile row owned by this thread
-    const int ptid = threadIdx.x - 64;
+    const int ptid = threadIdx.x - 32 * kFirstPromoWarp;
     const uint32_t t_lane = static_cast<uint32_t>(32 * q) << 16;
     uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const Tile T = decode_tile(t, tab_tile, tab_row, tab_size, tab_crow, G);
+    for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+      const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int rp = sa_row_prev(T.row0, rb);
       const float* sbp = p.sb + (p.b_shared ? 0 : static_cast<int64_t>(T.g) * p.sb_sg) +
-                         static_cast<int64_t>(T.n0 >> 7) * p.sb_snb;
+                         static_cast<int64_t>((T.n0 + half * kCPT) >> 7) * p.sb_snb;
       mbar_wait(&safull[sab], saph);
       const float* sa_row = reinterpret_cast<const float*>(sSA + sab * p.sa_buf_bytes +
                                                            static_cast<uint32_t>(rp + r) * rb);
-      float acc[64];
+      float acc[kCPT];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
+      for (int i = 0; i < kCPT; ++i) acc[i] = 0.0f;
       float sb_next = __ldg(sbp);
       for (int kb = 0; kb < kbc; ++kb) {
         const float sbv = sb_next;
@@ -272,76 +355,113 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         const float s = __fmul_rn(sa_row[kb], sbv);
         mbar_wait(&tfull[acc_i], accph);
         tc_fence_after();
-        uint32_t v0[32], v1[32];
-        const uint32_t taddr = tmem_base + t_lane + acc_i * BN + half * 64;
-        tmem_ld_32x32b_x32(taddr, v0);
-        tmem_ld_32x32b_x32(taddr + 32, v1);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc_i]);
-        if (++acc_i == kNumAcc) { acc_i = 0; accph ^= 1; }
-        if constexpr (kExact) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            acc[i] = __fadd_rn(acc[i], __fmul_rn(__uint_as_float(v0[i]), s));
-            acc[32 + i] = __fadd_rn(acc[32 + i], __fmul_rn(__uint_as_float(v1[i]), s));
+        if (p.dbg & kDbgNoPromote) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (kCG == 1) mbar_arrive(&tempty[acc_i]); else mbar_arrive_leader(&tempty[acc_i]);
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            ffma2(acc[i], acc[i + 1], __uint_as_float(v0[i]), __uint_as_float(v0[i + 1]), s);
-            ffma2(acc[32 + i], acc[33 + i], __uint_as_float(v1[i]), __uint_as_float(v1[i + 1]), s);
-          }
+          if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
+          acc[0] += s;
+          continue;
         }
+        const uint32_t taddr = tmem_base + t_lane + acc_i * C::kBN + half * kCPT;
+        // Software-pipelined TMEM drain: chunk c+1 is in flight while chunk c is
+        // promoted; the buffer is handed back as soon as the last chunk has landed.
+        constexpr int kChunks = kCPT / 32;
+        uint32_t va[32], vb[32];
+        tmem_ld_32x32b_x32(taddr, va);
+        tmem_wait_ld_dep(va);
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c) {
+          uint32_t(&cur)[32] = (c & 1) ? vb : va;
+          uint32_t(&nxt)[32] = (c & 1) ? va : vb;
+          if (c + 1 < kChunks) {
+            tmem_ld_32x32b_x32(taddr + 32 * (c + 1), nxt);
+          } else {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (kCG == 1) mbar_arrive(&tempty[acc_i]); else mbar_arrive_leader(&tempty[acc_i]);
+            }
+          }
+          if constexpr (kExact) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              acc[32 * c + i] = __fadd_rn(acc[32 * c + i], __fmul_rn(__uint_as_float(cur[i]), s));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2)
+              ffma2(acc[32 * c + i], acc[32 * c + i + 1], __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]), s);
+          }
+          if (c + 1 < kChunks) tmem_wait_ld_dep(nxt);
+        }
+        if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&saempty[sab]);
       if (++sab == 2) { sab = 0; saph ^= 1; }
 
-      // ---- epilogue: bf16 -> smem staging -> TMA store (pool + dual phase)
-      if (ptid == 0) bulk_wait_read0();  // previous tile's stores have read the staging
-      named_bar_sync(1, 32 * kNumPromoWarps);
-      const uint32_t row_addr = smem_u32(sC + half * kChunkBytesC) + static_cast<uint32_t>(r) * 128u;
+      // ---- epilogue: bf16 -> swizzled smem staging (2 chunks of 64 columns)
+      //      -> TMA stores from the 8-height pool, dual phase for residual rows.
+      //      kBN=128: one pass, warp half h writes chunk h (its 64 columns).
+      //      kBN=256: pass h, warp half h writes both chunks (its 128 columns).
+      const int lg = T.valid > 0 ? 31 - __clz(T.valid) : 0;  // pool index: d = 2^floor(log2 valid)
+      const int d = 1 << lg;
+      constexpr int kPasses = kBN / 128;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t w0 = pack_bf16x2(acc[8 * j + 0], acc[8 * j + 1]);
-        const uint32_t w1 = pack_bf16x2(acc[8 * j + 2], acc[8 * j + 3]);
-        const uint32_t w2 = pack_bf16x2(acc[8 * j + 4], acc[8 * j + 5]);
-        const uint32_t w3 = pack_bf16x2(acc[8 * j + 6], acc[8 * j + 7]);
-        const uint32_t c16 = kSwizzleC ? static_cast<uint32_t>(j ^ (r & 7)) : static_cast<uint32_t>(j);
-        st_shared_v4(row_addr + c16 * 16u, w0, w1, w2, w3);
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(1, 32 * kNumPromoWarps);
-      if (ptid == 0) {
-        const int lg = 31 - __clz(T.valid);  // pool index: d = 2^floor(log2 valid)
-        const int d = 1 << lg;
-        for (int h = 0; h < 2; ++h) {
-          const int col = T.n0 + 64 * h;
-          if (col >= p.N) break;
-          const uint8_t* chunk = sC + h * kChunkBytesC;
-          // phase a: smem rows [0, d) -> rows [crow0, crow0 + d)
-          tma_store_2d(&p.tmap_c[lg], chunk, col, T.crow0);
-          // phase b: smem rows [valid - d, valid) -> rows [crow0 + valid - d, crow0 + valid)
-          // (for a full tile, or a power-of-two residual, both phases coincide:
-          // a full tile issues one store, as engine.py:318-322 does)
-          if (T.valid != BM)
-            tma_store_2d(&p.tmap_c[lg], chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
-                         T.crow0 + T.valid - d);
+      for (int pass = 0; pass < kPasses; ++pass) {
+        if (ptid == 0) bulk_wait_read0();  // earlier stores have finished reading the staging
+        named_bar_sync(1, 32 * kNumPromoWarps);
+        if (kCPT == 64 || half == pass) {
+#pragma unroll
+          for (int j = 0; j < kCPT / 8; ++j) {
+            const int chunk = (kCPT == 64) ? half : (j >> 3);
+            const int pc = j & 7;
+            const uint32_t w0 = pack_bf16x2(acc[8 * j + 0], acc[8 * j + 1]);
+            const uint32_t w1 = pack_bf16x2(acc[8 * j + 2], acc[8 * j + 3]);
+            const uint32_t w2 = pack_bf16x2(acc[8 * j + 4], acc[8 * j + 5]);
+            const uint32_t w3 = pack_bf16x2(acc[8 * j + 6], acc[8 * j + 7]);
+            const uint32_t c16 = kSwizzleC ? static_cast<uint32_t>(pc ^ (r & 7)) : static_cast<uint32_t>(pc);
+            st_shared_v4(smem_u32(sC + chunk * kChunkBytesC) + static_cast<uint32_t>(r) * 128u + c16 * 16u, w0, w1,
+                         w2, w3);
+          }
+          fence_proxy_async_smem();
         }
-        bulk_commit();
-        if (p.tile_map) {
-          int32_t* rec = p.tile_map + static_cast<int64_t>(t) * TAGG_TILE_MAP_FIELDS;
-          rec[0] = T.g;
-          rec[1] = T.mt;
-          rec[2] = T.n0;
-          rec[3] = T.row0;
-          rec[4] = T.valid;
-          rec[5] = d;
-          rec[6] = T.crow0;
-          rec[7] = T.valid - d;
-          rec[8] = T.crow0 + T.valid - d;
+        named_bar_sync(1, 32 * kNumPromoWarps);
+        if (ptid == 0 && T.valid > 0) {
+          for (int ch = 0; ch < 2; ++ch) {
+            const int col = T.n0 + 128 * pass + 64 * ch;
+            if (col >= p.N) break;
+            const uint8_t* chunk = sC + ch * kChunkBytesC;
+            // phase a: smem rows [0, d) -> rows [crow0, crow0 + d)
+            tma_store_2d(&p.tmap_c[lg], chunk, col, T.crow0);
+            // phase b: smem rows [valid - d, valid) -> rows [crow0 + valid - d, crow0 + valid).
+            // A full tile is one store (engine.py:318-322); a residual tile issues both
+            // phases even when they coincide (descriptors.py:14-16).
+            if (T.valid != BM)
+              tma_store_2d(&p.tmap_c[lg], chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
+                           T.crow0 + T.valid - d);
+          }
+          bulk_commit();
+          if (p.tile_map) {
+            for (int sub = 0; sub < C::kBN / 128; ++sub) {
+              if (sub != pass) continue;
+              const int n0 = T.n0 + 128 * sub;
+              if (n0 >= p.N) continue;
+              int32_t* rec = p.tile_map + ((static_cast<int64_t>(t) * kCG + rank) * (C::kBN / 128) + sub) *
+                                              TAGG_TILE_MAP_FIELDS;
+              rec[0] = T.g;
+              rec[1] = T.mt;
+              rec[2] = n0;
+              rec[3] = T.row0;
+              rec[4] = T.valid;
+              rec[5] = d;
+              rec[6] = T.crow0;
+              rec[7] = T.valid - d;
+              rec[8] = T.crow0 + T.valid - d;
+            }
+          }
         }
       }
     }
@@ -349,11 +469,12 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   }
 
   // ------------------------------------------------------------ teardown
-  __syncthreads();
+  __syncwarp();
+  tc_fence_before();
+  if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
-    __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, kTmemCols);
+    tmem_dealloc<kCG>(tmem_base, kTmemCols);
   }
 }
 
@@ -417,7 +538,7 @@ int gcd_int(int a, int b) {
 }  // namespace
 
 // Smem layout for a given stage count; returns total bytes (incl. alignment slack).
-static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb) {
+static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_acc, uint32_t stage_bytes_b) {
   // row_prev < 16 / gcd(rb, 16): the residue class of row0*rb mod 16 has that period
   const int rp_max = 16 / gcd_int(rb, 16) - 1;
   const uint32_t sa_buf = align_up(static_cast<uint32_t>(((rp_max + BM) * rb + 15) & ~15), 128);
@@ -425,35 +546,65 @@ static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb) {
   p.sa_buf_bytes = sa_buf;
   p.off_a = 0;
   p.off_b = stages * kStageBytesA;
-  p.off_c = p.off_b + stages * kStageBytesB;
+  p.off_c = p.off_b + stages * stage_bytes_b;
   p.off_sa = p.off_c + kCStagingBytes;
   p.off_tab = p.off_sa + 2 * sa_buf;
   const uint32_t tab_bytes = align_up(4u * static_cast<uint32_t>(2 * (G + 1) + 2 * G), 16);
   p.off_bar = p.off_tab + tab_bytes;
-  const uint32_t bar_bytes = (2 * stages + 2 * kNumAcc + 4) * 8 + 16;
+  const uint32_t bar_bytes = (2 * stages + 2 * num_acc + 4) * 8 + 16;
   return p.off_bar + bar_bytes + 1024;
 }
 
-template <bool kExact, bool kSwizzleC>
+template <int kCG, int kBN, bool kExact, bool kSwizzleC>
 static cudaError_t launch(const Params& p, uint32_t smem_bytes, int grid, cudaStream_t stream) {
-  auto kern = tagg_gemm_kernel<kExact, kSwizzleC>;
-  static uint32_t configured = 0;  // max dynamic smem already granted to this instance
-  if (smem_bytes > configured) {
+  auto kern = tagg_gemm_kernel<kCG, kBN, kExact, kSwizzleC>;
+  static bool configured = false;
+  if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
-    configured = 232448;
+    configured = true;
   }
-  kern<<<grid, kThreads, smem_bytes, stream>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <int kCG, int kBN>
+static cudaError_t launch_cfg(const Params& p, uint32_t smem_bytes, int grid, cudaStream_t st, bool exact, bool swz) {
+  if (exact)
+    return swz ? launch<kCG, kBN, true, true>(p, smem_bytes, grid, st)
+               : launch<kCG, kBN, true, false>(p, smem_bytes, grid, st);
+  return swz ? launch<kCG, kBN, false, true>(p, smem_bytes, grid, st)
+             : launch<kCG, kBN, false, false>(p, smem_bytes, grid, st);
+}
+
+// Waves efficiency of a persistent schedule: tiles / (slots * ceil(tiles / slots)).
+static double wave_eff(double tiles, int slots) {
+  if (tiles <= 0) return 1.0;
+  const double w = tiles / slots;
+  return w / static_cast<double>(static_cast<int64_t>(w) + (w > static_cast<int64_t>(w) ? 1 : 0));
 }
 
 }  // namespace tagg
 
 using namespace tagg;
 
+// Capacity (records) a tile_map buffer needs: an upper bound valid for every
+// tile shape (one record per 128-row x 128-column store tile, incl. empty pair halves).
 extern "C" int64_t tagg_max_tiles(int64_t m_alloc, int G, int N) {
   if (m_alloc < 0 || G < 1 || N < 1) return 0;
-  return ((m_alloc + BM - 1) / BM + G) * ((N + BN - 1) / BN);
+  return ((m_alloc + 255) / 256 + G) * 2 * ((N + 255) / 256) * 2;
 }
 
 extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa, int64_t m_alloc,
@@ -477,6 +628,25 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   if (m_alloc == 0 || c_rows == 0) return TAGG_OK;  // nothing can be stored
   if (m_alloc >= (int64_t(1) << 31) || c_rows >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
 
+  const int sms = num_sms_for_current_device();
+  if (sms <= 0) return TAGG_ERR_CUDA;
+  // ---- tile shape: 1-CTA 128x128, or a CTA pair with a 256x256 / 256x128 tile.
+  // Without an explicit choice, the pair tile with the better wave efficiency
+  // (estimated from m_alloc and G, no device data) wins, preferring N=256.
+  int cg = 2, bn = 256;
+  if (flags & TAGG_FLAG_SINGLE_CTA) {
+    cg = 1;
+    bn = 128;
+  } else if (flags & TAGG_FLAG_TILE_N128) {
+    bn = 128;
+  } else if (!(flags & TAGG_FLAG_TILE_N256)) {
+    const double mt = (static_cast<double>(m_alloc) + 128.0 * G) / 256.0;  // expected pair m-tiles
+    const double e256 = wave_eff(mt * ((N + 255) / 256), sms / 2);
+    const double e128 = wave_eff(mt * ((N + 127) / 128), sms / 2);
+    if (e128 > e256 + 0.05) bn = 128;
+  }
+  const int num_acc = 512 / bn;
+  const uint32_t stage_bytes_b = static_cast<uint32_t>(BK * (bn / cg));
   const int kb_count = (K + BK - 1) / BK;
   const int rb = 4 * kb_count;
   Params p;
@@ -494,15 +664,16 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   p.N = N;
   p.K = K;
   p.kb_count = kb_count;
-  p.n_tiles = (N + BN - 1) / BN;
+  p.n_tiles = (N + bn - 1) / bn;
   p.sa_rb = rb;
   p.b_kmajor = (b_layout == TAGG_B_NK) ? 1 : 0;
   p.b_shared = (b_experts == 1) ? 1 : 0;
+  p.dbg = flags & (kDbgNoLoad | kDbgNoPromote);
 
   uint32_t smem_bytes = 0;
   uint32_t stages = kMaxStages;
   for (; stages >= 2; --stages) {
-    smem_bytes = smem_layout(p, stages, G, rb);
+    smem_bytes = smem_layout(p, stages, G, rb, num_acc, stage_bytes_b);
     if (smem_bytes <= 232448) break;
   }
   if (stages < 2) return TAGG_ERR_UNSUPPORTED;
@@ -517,16 +688,20 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   }
   {
     uint64_t dims[3], str[2];
-    const uint32_t box[3] = {128, 128, 1};
+    const uint32_t bcols = static_cast<uint32_t>(bn / cg);  // B columns per CTA
+    uint32_t box[3];
+    CUtensorMapSwizzle bsw = CU_TENSOR_MAP_SWIZZLE_128B;
     if (b_layout == TAGG_B_KN) {
       dims[0] = N; dims[1] = K; dims[2] = b_experts;
       str[0] = N; str[1] = static_cast<uint64_t>(K) * N;
+      box[0] = bcols; box[1] = 128; box[2] = 1;
+      if (bcols == 64) bsw = CU_TENSOR_MAP_SWIZZLE_64B;
     } else {
       dims[0] = K; dims[1] = N; dims[2] = b_experts;
       str[0] = K; str[1] = static_cast<uint64_t>(K) * N;
+      box[0] = 128; box[1] = bcols; box[2] = 1;
     }
-    if (!encode(&p.tmap_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, b, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
-      return TAGG_ERR_CUDA;
+    if (!encode(&p.tmap_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, b, dims, str, box, bsw)) return TAGG_ERR_CUDA;
   }
   const bool swz = (flags & TAGG_FLAG_PLAIN_C_STAGING) == 0;
   for (int i = 0; i < kPoolSize; ++i) {
@@ -538,17 +713,15 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
       return TAGG_ERR_CUDA;
   }
 
-  const int sms = num_sms_for_current_device();
-  if (sms <= 0) return TAGG_ERR_CUDA;
-  const int64_t max_tiles = tagg_max_tiles(m_alloc, G, N);
-  const int grid = static_cast<int>(std::min<int64_t>(sms, max_tiles));
+  // persistent grid: one CTA (cg=1) or CTA pair (cg=2) per SM (pair), capped by the tile bound
+  const int64_t tile_bound = ((m_alloc + 128 * cg - 1) / (128 * cg) + G) * p.n_tiles;  // scheduled tiles
+  const int grid = static_cast<int>(std::min<int64_t>(sms / cg, tile_bound)) * cg;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool exact = (flags & TAGG_FLAG_EXACT_PROMOTION) != 0;
   cudaError_t e;
-  if (exact)
-    e = swz ? launch<true, true>(p, smem_bytes, grid, st) : launch<true, false>(p, smem_bytes, grid, st);
-  else
-    e = swz ? launch<false, true>(p, smem_bytes, grid, st) : launch<false, false>(p, smem_bytes, grid, st);
+  if (cg == 1) e = launch_cfg<1, 128>(p, smem_bytes, grid, st, exact, swz);
+  else if (bn == 128) e = launch_cfg<2, 128>(p, smem_bytes, grid, st, exact, swz);
+  else e = launch_cfg<2, 256>(p, smem_bytes, grid, st, exact, swz);
   if (e != cudaSuccess) {
     std::fprintf(stderr, "tagg_grouped_gemm_fp8: launch failed: %s\n", cudaGetErrorString(e));
     return TAGG_ERR_CUDA;

@@ -29,6 +29,10 @@ from .errors import ConfigError, InvalidBlockM, InvalidBlockN, ShapeMismatch, ra
 K_BLOCK = 128
 FLAG_EXACT_PROMOTION = 1
 FLAG_PLAIN_C_STAGING = 2
+FLAG_SINGLE_CTA = 4
+FLAG_TILE_N128 = 8
+FLAG_TILE_N256 = 16
+TILES = {None: 0, "auto": 0, "1cta": FLAG_SINGLE_CTA, "pair_n128": FLAG_TILE_N128, "pair_n256": FLAG_TILE_N256}
 TILE_MAP_FIELDS = 9
 
 
@@ -169,7 +173,8 @@ def _ptr(t):
 
 
 def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", out=None, c_row_offsets=None,
-                     tile_map=None, exact_promotion=False, plain_staging=False, stream=None):
+                     tile_map=None, exact_promotion=False, plain_staging=False, single_cta=False, tile=None,
+                     stream=None):
     """Padding-free FP8 grouped GEMM on device tensors (no host sync).
 
     a [m_alloc,K] uint8 / float8_e4m3fn; a_scales [m_alloc,ceil(K/128)] f32;
@@ -177,7 +182,8 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
     [G,kb,nb] / [G,nb,kb]; group_sizes int32 CUDA tensor [G] (sum <= m_alloc).
     Returns ``out`` (bf16 [c_rows, N]).  Only rows of valid group rows are
     written; with ``c_row_offsets`` (int64 CUDA [G]) group g's rows start at
-    c_row_offsets[g].
+    c_row_offsets[g].  ``tile`` picks the tile shape: "pair_n256" (CTA pair,
+    256x256), "pair_n128" (CTA pair, 256x128), "1cta" (128x128) or None/"auto".
     """
     if not (isinstance(a, torch.Tensor) and a.is_cuda):
         raise ValueError("grouped_gemm_fp8 expects CUDA tensors (no CPU fallback)")
@@ -227,7 +233,8 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
         raise ShapeMismatch("out must be a row-major bf16 [c_rows, N] tensor")
     if c_row_offsets is not None and (c_row_offsets.dtype != torch.int64 or not c_row_offsets.is_cuda):
         raise ShapeMismatch("c_row_offsets must be an int64 CUDA tensor")
-    flags = (FLAG_EXACT_PROMOTION if exact_promotion else 0) | (FLAG_PLAIN_C_STAGING if plain_staging else 0)
+    flags = ((FLAG_EXACT_PROMOTION if exact_promotion else 0) | (FLAG_PLAIN_C_STAGING if plain_staging else 0)
+             | (FLAG_SINGLE_CTA if single_cta else 0) | TILES[tile])
     st = stream if stream is not None else torch.cuda.current_stream(a.device)
     rc = lib().tagg_grouped_gemm_fp8(
         _ptr(a), a.stride(0), _ptr(a_scales), m_alloc, _ptr(b), layout, b_experts, _ptr(b_scales),
@@ -319,7 +326,8 @@ def _device_operands(config: ProblemConfig, operands: GroupedOperands, device):
 
 
 def run_adaptive(config: ProblemConfig, operands: GroupedOperands, *, poison: int = 0xA5,
-                 device="cuda", exact_promotion=False, plain_staging=False) -> AdaptiveRun:
+                 device="cuda", exact_promotion=False, plain_staging=False, single_cta=False,
+                 tile=None) -> AdaptiveRun:
     """engine.py:184-343 on the GPU: one launch of the padding-free kernel.
 
     C is pre-filled with the ``poison`` byte pattern before the launch, so any
@@ -334,7 +342,8 @@ def run_adaptive(config: ProblemConfig, operands: GroupedOperands, *, poison: in
     if m:
         tmap = torch.full((max_tiles(m, config.groups, n), TILE_MAP_FIELDS), -1, dtype=torch.int32, device=device)
         grouped_gemm_fp8(a, sa, b, sb, gs, b_layout=operands.b_layout, out=c, tile_map=tmap,
-                         exact_promotion=exact_promotion, plain_staging=plain_staging)
+                         exact_promotion=exact_promotion, plain_staging=plain_staging, single_cta=single_cta,
+                         tile=tile)
     c_bits = c.cpu().numpy().view(np.uint16) if m else np.zeros((0, n), dtype=np.uint16)
     tm = None
     if tmap is not None:

@@ -32,21 +32,25 @@ def _cfg_ops(case):
 
 
 @pytest.mark.parametrize("name", CASES)
-@pytest.mark.parametrize("mode", ["ffma2", "exact", "plain_staging"])
+@pytest.mark.parametrize("mode", ["ffma2", "exact", "plain_staging", "1cta", "1cta_exact", "pair_n128",
+                                  "pair_n128_exact", "pair_n256"])
 def test_golden_fixtures(name, mode):
     case = load_case(name)
     cfg, ops, _ = _cfg_ops(case)
-    run = tg.run_adaptive(cfg, ops, exact_promotion=(mode == "exact"), plain_staging=(mode == "plain_staging"))
+    tile = next((t for t in ("1cta", "pair_n128", "pair_n256") if mode.startswith(t)), None)
+    run = tg.run_adaptive(cfg, ops, exact_promotion=("exact" in mode), plain_staging=(mode == "plain_staging"),
+                          tile=tile)
     rep = assert_parity(run.c_bits, case["c_golden"], label=f"{name}/{mode}")
     print(f"{name}/{mode}: {rep}")
 
 
 @pytest.mark.parametrize("name", CASES)
-def test_tile_map_is_bit_exact(name):
+@pytest.mark.parametrize("tile", ["1cta", "pair_n128", "pair_n256"])
+def test_tile_map_is_bit_exact(name, tile):
     """The store geometry the kernel used equals the reference tile loop (engine.py:269-335)."""
     case = load_case(name)
     cfg, ops, _ = _cfg_ops(case)
-    run = tg.run_adaptive(cfg, ops)
+    run = tg.run_adaptive(cfg, ops, tile=tile)
     got = sorted(tuple(int(x) for x in r) for r in run.tile_map)
     want = sorted(oplan.tile_map(cfg.group_sizes, cfg.n))
     assert got == want
@@ -76,7 +80,8 @@ def _dev(x, dtype=None):
 
 
 @pytest.mark.parametrize("gap", [1, 3, 128])
-def test_untouched_memory_between_groups(gap):
+@pytest.mark.parametrize("tile", ["1cta", "pair_n128", "pair_n256"])
+def test_untouched_memory_between_groups(gap, tile):
     """No row beyond M_g is ever written: sentinel rows between groups survive."""
     sizes = (1, 67, 128, 255, 0, 129, 200, 64, 3)
     n, k = 192, 384
@@ -88,7 +93,7 @@ def test_untouched_memory_between_groups(gap):
     sentinel = 0x7BCD
     out = torch.full((o, n), sentinel, dtype=torch.int16, device=DEV)
     tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
-                        out=out, c_row_offsets=_dev(np.array(offs, np.int64)))
+                        out=out, c_row_offsets=_dev(np.array(offs, np.int64)), tile=tile)
     got = out.cpu().numpy().view(np.uint16)
     want = oracle_c(ac, asc, bc, bsc, sizes)
     a = 0
@@ -98,14 +103,15 @@ def test_untouched_memory_between_groups(gap):
         a += s
 
 
-def test_residual_sweep_every_residue_small():
-    """Every M_g mod 128 in 1..127 (configs[1] pattern, M_g = 128*g + r) at N=128, K=256."""
-    n, k = 128, 256
+@pytest.mark.parametrize("tile", ["1cta", "pair_n128", "pair_n256"])
+def test_residual_sweep_every_residue_small(tile):
+    """Every M_g mod 128 in 1..127 (configs[1] pattern, M_g = 128*g + r) at N=256, K=256."""
+    n, k = 256, 256
     for r0 in range(1, 128, 16):
         sizes = tuple(128 * g + ((r0 + g) % 127 + 1) for g in range(8))
         ac, asc, bc, bsc = per_expert_operands(sizes, n, k, r0)
         cfg = tg.ProblemConfig(n=n, k=k, group_sizes=sizes)
-        run = tg.run_adaptive(cfg, tg.GroupedOperands(ac, asc, bc, bsc))
+        run = tg.run_adaptive(cfg, tg.GroupedOperands(ac, asc, bc, bsc), tile=tile)
         assert_parity(run.c_bits, oracle_c(ac, asc, bc, bsc, sizes), label=f"r0={r0}")
         got = sorted(tuple(int(x) for x in rr) for rr in run.tile_map)
         assert got == sorted(oplan.tile_map(sizes, n))
@@ -136,14 +142,15 @@ def _synthetic(sizes, n, k, seed, layout="kn"):
 
 
 @pytest.mark.parametrize("layout", ["kn", "nk"])
-def test_deepseek_shape_sampled_columns(layout):
+@pytest.mark.parametrize("tile", ["1cta", "pair_n128", "pair_n256"])
+def test_deepseek_shape_sampled_columns(layout, tile):
     """DeepSeek-V3 gate+up shape (N=4096, K=7168) with ragged groups.  Parity is
     checked on two 128-column slices and all rows against the oracle."""
     sizes = (300, 0, 1, 1024, 77, 513, 128, 255)
     n, k = 4096, 7168
     ac, asc, bc, bsc = _synthetic(sizes, n, k, 7, layout)
     out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
-                              b_layout=layout)
+                              b_layout=layout, tile=tile)
     got = out.view(torch.int16).cpu().numpy().view(np.uint16)
     for n0 in (0, 2944):
         want = np.zeros((sum(sizes), n), dtype=np.uint16)
@@ -152,11 +159,13 @@ def test_deepseek_shape_sampled_columns(layout):
         print(f"deepseek {layout} n0={n0}: {rep}")
 
 
-def test_k_tail_and_n_tail_shapes():
-    sizes = (5, 130, 37)
-    for n, k in ((64, 16), (192, 208), (320, 1664), (64, 4112)):
+@pytest.mark.parametrize("tile", ["1cta", "pair_n128", "pair_n256"])
+def test_k_tail_and_n_tail_shapes(tile):
+    sizes = (5, 130, 37, 300)
+    for n, k in ((64, 16), (192, 208), (320, 1664), (64, 4112), (448, 640)):
         ac, asc, bc, bsc = _synthetic(sizes, n, k, n + k)
-        out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)))
+        out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
+                                  tile=tile)
         got = out.view(torch.int16).cpu().numpy().view(np.uint16)
         assert_parity(got, oracle_c(ac, asc, bc, bsc, sizes), label=f"n={n} k={k}")
 
