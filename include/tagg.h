@@ -54,8 +54,7 @@ extern "C" {
                                         default CTA-pair tile (cta_group::2) */
 #define TAGG_FLAG_TILE_N128 8u       /* CTA-pair tile 256x128 (more, smaller tiles: fewer idle SMs
                                         in the last wave of small problems) */
-#define TAGG_FLAG_TILE_N256 16u      /* CTA-pair tile 256x256 (half the operand traffic per FLOP);
-                                        without either flag the launcher picks by wave efficiency */
+#define TAGG_FLAG_TILE_N256 16u      /* CTA-pair tile 256x256 (the default) */
 
 #define TAGG_TILE_MAP_FIELDS 9
 

@@ -589,12 +589,6 @@ static cudaError_t launch_cfg(const Params& p, uint32_t smem_bytes, int grid, cu
              : launch<kCG, kBN, false, false>(p, smem_bytes, grid, st);
 }
 
-// Waves efficiency of a persistent schedule: tiles / (slots * ceil(tiles / slots)).
-static double wave_eff(double tiles, int slots) {
-  if (tiles <= 0) return 1.0;
-  const double w = tiles / slots;
-  return w / static_cast<double>(static_cast<int64_t>(w) + (w > static_cast<int64_t>(w) ? 1 : 0));
-}
 
 }  // namespace tagg
 
@@ -630,20 +624,16 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
 
   const int sms = num_sms_for_current_device();
   if (sms <= 0) return TAGG_ERR_CUDA;
-  // ---- tile shape: 1-CTA 128x128, or a CTA pair with a 256x256 / 256x128 tile.
-  // Without an explicit choice, the pair tile with the better wave efficiency
-  // (estimated from m_alloc and G, no device data) wins, preferring N=256.
+  // ---- tile shape: the CTA-pair 256x256 tile by default (half the operand
+  // traffic per FLOP of 256x128; measured faster even on the residual sweep,
+  // whose 320 pair tiles leave the last of 5 waves 32% full), or an explicit
+  // 256x128 pair tile / 1-CTA 128x128 tile.
   int cg = 2, bn = 256;
   if (flags & TAGG_FLAG_SINGLE_CTA) {
     cg = 1;
     bn = 128;
   } else if (flags & TAGG_FLAG_TILE_N128) {
     bn = 128;
-  } else if (!(flags & TAGG_FLAG_TILE_N256)) {
-    const double mt = (static_cast<double>(m_alloc) + 128.0 * G) / 256.0;  // expected pair m-tiles
-    const double e256 = wave_eff(mt * ((N + 255) / 256), sms / 2);
-    const double e128 = wave_eff(mt * ((N + 127) / 128), sms / 2);
-    if (e128 > e256 + 0.05) bn = 128;
   }
   const int num_acc = 512 / bn;
   const uint32_t stage_bytes_b = static_cast<uint32_t>(BK * (bn / cg));
