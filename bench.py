@@ -410,6 +410,8 @@ def main():
     extra = {}
     if not args.no_extra:
         extra = run_extra(torch, tg, dev, rank, fp8_peak, args.exact)
+    if world > 1:
+        extra["deepseek_v3_down_ep"] = run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, args.exact)
 
     if rank != 0:
         if world > 1:
@@ -446,7 +448,8 @@ def main():
                      "frac": achieved / fp8_peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "peak_source": f"fp8 dense = 2 x bf16_tflops ({peaks_src})",
-                     "kernel": "tagg_gemm_kernel<false,true>" if not args.exact else "tagg_gemm_kernel<true,true>"},
+                     "kernel": f"tagg_gemm_kernel<2, 256, {int(args.exact)}, 1> (CTA pair, 256x256 tile)",
+                     "traffic_source": "profiles/traffic_residual_sweep.json (ncu launch list, mean per launch)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "note": "A, S_A, group sizes H2D from pinned memory and every C D2H each step; expert weights resident"},
@@ -486,6 +489,73 @@ def run_extra(torch, tg, dev, rank, fp8_peak, exact):
         del P
         torch.cuda.empty_cache()
     return out
+
+
+def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, warmup=2):
+    """BASELINE.json configs[3]: DeepSeek-V3 down proj (N=7168, K=2048), 256 experts
+    sharded over the ranks, 32768 tokens x top-8 (strong scaling: each rank
+    routes 32768/world tokens).  NCCL all_to_all dispatch of the FP8 rows +
+    scales, then the padding-free grouped GEMM on the rank's experts.  Device
+    time is measured with events and the max is taken over ranks."""
+    from paper_2508_16584_b200 import ep
+
+    E, N, K, topk, tokens = 256, 7168, 2048, 8, 32768
+    epr = E // world
+    t_local = tokens // world
+    g = torch.Generator(device=dev).manual_seed(4242)  # same popularity map on every rank
+    logp = -0.8 * torch.log(torch.randperm(E, device=dev, generator=g).float() + 1)
+    gr = torch.Generator(device=dev).manual_seed(100 + rank)
+    gumbel = -torch.log(-torch.log(torch.rand((t_local, E), device=dev, generator=gr).clamp_min(1e-20)))
+    eid = torch.topk(logp[None, :] + gumbel, topk, dim=1).indices.reshape(-1)
+    rows = eid.numel()
+    a = _codes(torch, (rows, K), gr, dev)
+    sa = _scales(torch, (rows, K // 128), gr, dev)
+    b = _codes(torch, (epr, K, N), gr, dev)
+    sb = _scales(torch, (epr, K // 128, N // 128), gr, dev)
+    state = {}
+
+    def dispatch():
+        state["a"], state["sa"], state["meta"] = ep.dispatch(a, sa, eid, E)
+
+    def gemm():
+        m = state["a"].shape[0]
+        if "out" not in state or state["out"].shape[0] < m:
+            state["out"] = torch.empty((max(m, 1), N), dtype=torch.bfloat16, device=dev)
+        if m:
+            tg.grouped_gemm_fp8(state["a"], state["sa"], b, sb, state["meta"].group_sizes, out=state["out"],
+                                exact_promotion=exact)
+
+    for _ in range(warmup):
+        dispatch()
+        gemm()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_a2a = t_gemm = 0.0
+    for _ in range(iters):
+        ev[0].record()
+        dispatch()
+        ev[1].record()
+        gemm()
+        ev[2].record()
+        torch.cuda.synchronize()
+        t_a2a += ev[0].elapsed_time(ev[1])
+        t_gemm += ev[1].elapsed_time(ev[2])
+    local_rows = state["a"].shape[0]
+    flops_local = 2.0 * local_rows * N * K
+    stats = torch.tensor([t_a2a / iters, t_gemm / iters, flops_local, local_rows], dtype=torch.float64, device=dev)
+    mx = stats.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    tot = stats.clone()
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    a2a_ms, gemm_ms = float(mx[0]), float(mx[1])
+    return {"N": N, "K": K, "experts": E, "experts_per_rank": epr, "tokens": tokens, "topk": topk, "world": world,
+            "rows_total": int(tot[3]), "rows_max_rank": int(mx[3]),
+            "gemm_tflops_aggregate": float(tot[2]) / (gemm_ms * 1e-3) / 1e12,
+            "gemm_tflops_per_gpu_max_rank": float(mx[2]) / (gemm_ms * 1e-3) / 1e12,
+            "e2e_tflops_aggregate_incl_a2a": float(tot[2]) / ((gemm_ms + a2a_ms) * 1e-3) / 1e12,
+            "a2a_ms_max": a2a_ms, "gemm_ms_max": gemm_ms,
+            "a2a_bytes_per_row": K + 4 * (K // 128), "transport": "NCCL all_to_all_single (NVLink/NVSwitch)"}
 
 
 if __name__ == "__main__":

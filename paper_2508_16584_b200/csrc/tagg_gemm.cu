@@ -336,12 +336,14 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const int r = 32 * q + lane;     // tile row owned by this thread
     const int ptid = threadIdx.x - 32 * kFirstPromoWarp;
     const uint32_t t_lane = static_cast<uint32_t>(32 * q) << 16;
+    const bool no_promote = (p.dbg & kDbgNoPromote) != 0;
     uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int rp = sa_row_prev(T.row0, rb);
       const float* sbp = p.sb + (p.b_shared ? 0 : static_cast<int64_t>(T.g) * p.sb_sg) +
                          static_cast<int64_t>((T.n0 + half * kCPT) >> 7) * p.sb_snb;
+      const int64_t sb_step = p.sb_skb;
       mbar_wait(&safull[sab], saph);
       const float* sa_row = reinterpret_cast<const float*>(sSA + sab * p.sa_buf_bytes +
                                                            static_cast<uint32_t>(rp + r) * rb);
@@ -351,11 +353,12 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       float sb_next = __ldg(sbp);
       for (int kb = 0; kb < kbc; ++kb) {
         const float sbv = sb_next;
-        if (kb + 1 < kbc) sb_next = __ldg(sbp + static_cast<int64_t>(kb + 1) * p.sb_skb);
+        sbp += sb_step;
+        if (kb + 1 < kbc) sb_next = __ldg(sbp);
         const float s = __fmul_rn(sa_row[kb], sbv);
         mbar_wait(&tfull[acc_i], accph);
         tc_fence_after();
-        if (p.dbg & kDbgNoPromote) {
+        if (no_promote) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
