@@ -67,6 +67,7 @@ constexpr uint32_t kCStagingBytes = 2 * kChunkBytesC;
 constexpr int kPoolSize = 8;  // heights 1, 2, ..., 128 (descriptors.py:31-35)
 constexpr uint32_t kDbgNoLoad = 1u << 8;     // diagnostics: producer signals stages without loads
 constexpr uint32_t kDbgNoPromote = 1u << 9;  // diagnostics: promotion skips tcgen05.ld + math
+constexpr uint32_t kDbgNoMath = 1u << 10;    // diagnostics: promotion drains TMEM but skips the FFMA math
 
 struct Params {
   CUtensorMap tmap_a;
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const int ptid = threadIdx.x - 32 * kFirstPromoWarp;
     const uint32_t t_lane = static_cast<uint32_t>(32 * q) << 16;
     const bool no_promote = (p.dbg & kDbgNoPromote) != 0;
+    const bool no_math = (p.dbg & kDbgNoMath) != 0;
     uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
@@ -388,7 +390,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
               if constexpr (kCG == 1) mbar_arrive(&tempty[acc_i]); else mbar_arrive_leader(&tempty[acc_i]);
             }
           }
-          if constexpr (kExact) {
+          if (no_math) {
+            acc[32 * c] += __uint_as_float(cur[c]);
+          } else if constexpr (kExact) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               acc[32 * c + i] = __fadd_rn(acc[32 * c + i], __fmul_rn(__uint_as_float(cur[i]), s));
@@ -510,8 +514,59 @@ int num_sms_for_current_device() {
   return cached[dev];
 }
 
+// Encoded tensor maps are cached by their full description (a small direct-mapped
+// table): a steady-state call re-encodes nothing.
+struct MapKey {
+  uint64_t base, dims[3], strides[2];
+  uint32_t box[3], dt, rank, sw;
+  bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+struct MapEntry {
+  MapKey key;
+  CUtensorMap map;
+  bool valid;
+};
+constexpr int kMapCache = 64;
+MapEntry g_map_cache[kMapCache];
+std::mutex g_map_mu;
+
+bool encode_raw(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* base, const uint64_t* dims,
+                const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw);
+
 bool encode(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* base, const uint64_t* dims,
             const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw) {
+  MapKey k;
+  std::memset(&k, 0, sizeof(k));
+  k.base = reinterpret_cast<uint64_t>(base);
+  for (uint32_t i = 0; i < rank; ++i) {
+    k.dims[i] = dims[i];
+    k.box[i] = box[i];
+    if (i + 1 < rank) k.strides[i] = strides_bytes[i];
+  }
+  k.dt = static_cast<uint32_t>(dt);
+  k.rank = rank;
+  k.sw = static_cast<uint32_t>(sw);
+  uint64_t h = 1469598103934665603ull;
+  const unsigned char* kb = reinterpret_cast<const unsigned char*>(&k);
+  for (size_t i = 0; i < sizeof(k); ++i) h = (h ^ kb[i]) * 1099511628211ull;
+  MapEntry& e = g_map_cache[h % kMapCache];
+  {
+    std::lock_guard<std::mutex> lock(g_map_mu);
+    if (e.valid && e.key == k) {
+      *m = e.map;
+      return true;
+    }
+  }
+  if (!encode_raw(m, dt, rank, base, dims, strides_bytes, box, sw)) return false;
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  e.key = k;
+  e.map = *m;
+  e.valid = true;
+  return true;
+}
+
+bool encode_raw(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* base, const uint64_t* dims,
+                const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t d[5], s[4];
@@ -661,10 +716,12 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   p.sa_rb = rb;
   p.b_kmajor = (b_layout == TAGG_B_NK) ? 1 : 0;
   p.b_shared = (b_experts == 1) ? 1 : 0;
-  p.dbg = flags & (kDbgNoLoad | kDbgNoPromote);
+  p.dbg = flags & (kDbgNoLoad | kDbgNoPromote | kDbgNoMath);
 
   uint32_t smem_bytes = 0;
-  uint32_t stages = kMaxStages;
+  // bits 12-15 of flags cap the stage count (diagnostics); 0 = as many as fit
+  const uint32_t stage_cap = (flags >> 12) & 0xFu;
+  uint32_t stages = stage_cap ? std::min<uint32_t>(stage_cap, kMaxStages) : kMaxStages;
   for (; stages >= 2; --stages) {
     smem_bytes = smem_layout(p, stages, G, rb, num_acc, stage_bytes_b);
     if (smem_bytes <= 232448) break;

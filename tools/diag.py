@@ -11,9 +11,9 @@ res = {}
 for name, sizes, n, k, G in [("sweep_r64", [tuple(128 * g + 64 for g in range(8))], 4096, 7168, 8),
                              ("sq8192", [(8192,)], 8192, 8192, 1)]:
     P = Problem(torch, name, sizes, n, k, G, dev, seed=1)
-    for label, flags in [("n256", 16), ("n256_noload", 16 | 256), ("n256_noprom", 16 | 512),
-                         ("n256_neither", 16 | 256 | 512), ("n256_exact", 16 | 1),
-                         ("n128", 8), ("n128_neither", 8 | 256 | 512), ("1cta", 4), ("auto", 0)]:
+    variants = [("n256", 16), ("n256_nomath", 16 | 1024), ("n256_noprom", 16 | 512), ("n256_neither", 16 | 256 | 512),
+                ("n256_noload", 16 | 256), ("n256_noload_nomath", 16 | 256 | 1024), ("n256_exact", 16 | 1)]
+    for label, flags in variants + variants[:4]:  # second pass: compare against clock drift
         def run():
             rc = lib().tagg_grouped_gemm_fp8(P.a.data_ptr(), P.a.stride(0), P.sa.data_ptr(), P.m_alloc,
                                              P.b.data_ptr(), 0, G, P.sb.data_ptr(), P.sb.stride(0), P.sb.stride(1),
