@@ -36,6 +36,7 @@ SIGNATURES = {
     "tagg_pad_rows": (c_i64, [c_vp, c_int, c_i64]),
     "tagg_error_string": (ctypes.c_char_p, [c_int]),
     "tagg_version": (c_int, []),
+    "tagg_debug_trace": (None, [c_vp]),
 }
 
 _lib = None

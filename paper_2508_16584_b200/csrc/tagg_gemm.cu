@@ -78,6 +78,7 @@ struct Params {
   const int32_t* group_sizes;
   const int64_t* c_row_offsets;
   int32_t* tile_map;
+  unsigned long long* trace;  // diagnostics: per-event clock64 stamps of CTAs 0/1 (tagg_debug_trace)
   int64_t m_alloc;
   int64_t sb_sg, sb_skb, sb_snb;
   int32_t G, N, K, kb_count, n_tiles, sa_rb, b_kmajor, b_shared;
@@ -97,6 +98,19 @@ struct Cfg {
   static constexpr uint32_t kStageTx = kCG * (kStageBytesA + kStageBytesB);  // bytes landing per stage
   static_assert(kBCols == 64 || kBCols == 128, "B share per CTA must be 64 or 128 columns");
 };
+
+// Diagnostics trace: stamps of the first kTraceLen k-block iterations of CTAs 0 and 1.
+// Compiled in only with -DTAGG_TRACE (libtagg_trace.so, `make trace`; tools/trace.py).
+constexpr int kTraceLen = 1024;
+constexpr int kTraceEvents = 8;
+enum TraceEv { kEvMmaTempty = 0, kEvMmaFull, kEvMmaIssued, kEvProdEmpty, kEvPromoFull, kEvPromoFreed, kEvPromoDone,
+               kEvPromo2Full };
+__device__ __forceinline__ void trace_stamp(unsigned long long* tr, int ev, uint32_t i) {
+#ifdef TAGG_TRACE
+  if (tr != nullptr && blockIdx.x < 2 && i < static_cast<uint32_t>(kTraceLen))
+    tr[(blockIdx.x * kTraceEvents + ev) * kTraceLen + i] = clock64();
+#endif
+}
 
 struct Tile {
   int g, mt, n0, row0, valid, crow0;
@@ -233,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
    setmaxnreg_dec<kRegsControl>();
    if (warp == 0) {
     // ========================================================== TMA producer
-    uint32_t stage = 0, phase = 0, sab = 0, saph = 0;
+    uint32_t stage = 0, phase = 0, sab = 0, saph = 0, kiter = 0;
     const bool elected = elect_one();
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
@@ -263,6 +277,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       const int nb = T.n0 + rank * C::kBCols;
       for (int kb = 0; kb < kbc; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) trace_stamp(p.trace, kEvProdEmpty, kiter);  // no-op unless TAGG_TRACE
+        ++kiter;
         if (elected) {
           if (p.dbg & kDbgNoLoad) {
             if (is_leader) mbar_arrive(&full[stage]);
@@ -303,11 +319,13 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
                                          : umma_desc_sw64(smem_u32(sB), C::kStageBytesB, 512));
       const uint32_t b_kstep = p.b_kmajor ? (32u >> 4) : ((32u * C::kBCols) >> 4);  // desc units per K=32
       const bool elected = elect_one();
-      uint32_t stage = 0, phase = 0, acc = 0, accph = 0;
+      uint32_t stage = 0, phase = 0, acc = 0, accph = 0, kiter = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         for (int kb = 0; kb < kbc; ++kb) {
           mbar_wait(&tempty[acc], accph ^ 1);
+          if (lane == 0) trace_stamp(p.trace, kEvMmaTempty, kiter);
           mbar_wait(&full[stage], phase);
+          if (lane == 0) trace_stamp(p.trace, kEvMmaFull, kiter);
           tc_fence_after();
           if (elected) {
             const uint64_t ad = a_desc0 + ((stage * kStageBytesA) >> 4);
@@ -321,6 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             mma_commit<kCG>(&tfull[acc]);    // k-block partial ready for promotion (both CTAs)
           }
           __syncwarp();
+          if (lane == 0) trace_stamp(p.trace, kEvMmaIssued, kiter);
+          ++kiter;
           if (++stage == S) { stage = 0; phase ^= 1; }
           if (++acc == C::kNumAcc) { acc = 0; accph ^= 1; }
         }
@@ -339,7 +359,13 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t t_lane = static_cast<uint32_t>(32 * q) << 16;
     const bool no_promote = (p.dbg & kDbgNoPromote) != 0;
     const bool no_math = (p.dbg & kDbgNoMath) != 0;
-    uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0;
+    uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0;
+#ifdef TAGG_TRACE
+    const bool tr_a = p.trace != nullptr && pw == 0 && lane == 0;
+    const bool tr_b = p.trace != nullptr && pw == 4 && lane == 0;
+#else
+    constexpr bool tr_a = false, tr_b = false;
+#endif
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int rp = sa_row_prev(T.row0, rb);
@@ -347,8 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
                          static_cast<int64_t>((T.n0 + half * kCPT) >> 7) * p.sb_snb;
       const int64_t sb_step = p.sb_skb;
       mbar_wait(&safull[sab], saph);
-      const float* sa_row = reinterpret_cast<const float*>(sSA + sab * p.sa_buf_bytes +
-                                                           static_cast<uint32_t>(rp + r) * rb);
+      // this thread's S_A row in the over-fetched window
+      const uint32_t sa_row = smem_u32(sSA) + sab * p.sa_buf_bytes + static_cast<uint32_t>(rp + r) * rb;
       float acc[kCPT];
 #pragma unroll
       for (int i = 0; i < kCPT; ++i) acc[i] = 0.0f;
@@ -357,8 +383,10 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         const float sbv = sb_next;
         sbp += sb_step;
         if (kb + 1 < kbc) sb_next = __ldg(sbp);
-        const float s = __fmul_rn(sa_row[kb], sbv);
+        const float s = __fmul_rn(ld_shared_f32(sa_row + 4u * kb), sbv);
         mbar_wait(&tfull[acc_i], accph);
+        if (tr_a) trace_stamp(p.trace, kEvPromoFull, kiter);
+        if (tr_b) trace_stamp(p.trace, kEvPromo2Full, kiter);
         tc_fence_after();
         if (no_promote) {
           tc_fence_before();
@@ -367,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             if constexpr (kCG == 1) mbar_arrive(&tempty[acc_i]); else mbar_arrive_leader(&tempty[acc_i]);
           }
           if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
+          ++kiter;
           acc[0] += s;
           continue;
         }
@@ -389,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             if (lane == 0) {
               if constexpr (kCG == 1) mbar_arrive(&tempty[acc_i]); else mbar_arrive_leader(&tempty[acc_i]);
             }
+            if (tr_a) trace_stamp(p.trace, kEvPromoFreed, kiter);
           }
           if (no_math) {
             acc[32 * c] += __uint_as_float(cur[c]);
@@ -403,6 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           }
           if (c + 1 < kChunks) tmem_wait_ld_dep(nxt);
         }
+        if (tr_a) trace_stamp(p.trace, kEvPromoDone, kiter);
+        ++kiter;
         if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
       }
       __syncwarp();
@@ -622,13 +654,12 @@ static cudaError_t launch(const Params& p, uint32_t smem_bytes, int grid, cudaSt
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  cudaLaunchConfig_t cfg;
-  std::memset(&cfg, 0, sizeof(cfg));
+  cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[1] = {};
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kCG;
   attr[0].val.clusterDim.y = 1;
@@ -651,6 +682,14 @@ static cudaError_t launch_cfg(const Params& p, uint32_t smem_bytes, int grid, cu
 }  // namespace tagg
 
 using namespace tagg;
+
+namespace {
+unsigned long long* g_trace = nullptr;
+}
+
+// Diagnostics: the next launches stamp clock64 per k-block event of CTAs 0 and 1
+// into buf ([2][8][1024] u64, device); NULL turns tracing off.
+extern "C" void tagg_debug_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
 
 // Capacity (records) a tile_map buffer needs: an upper bound valid for every
 // tile shape (one record per 128-row x 128-column store tile, incl. empty pair halves).
@@ -704,6 +743,7 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   p.group_sizes = group_sizes;
   p.c_row_offsets = c_row_offsets;
   p.tile_map = tile_map;
+  p.trace = g_trace;
   p.m_alloc = m_alloc;
   p.sb_sg = sb_stride_g;
   p.sb_skb = sb_stride_kb;

@@ -1,0 +1,71 @@
+"""Pipeline trace of the GEMM kernel (diagnostics; needs libtagg_trace.so from `make -C
+paper_2508_16584_b200/csrc trace`).  Stamps clock64 at 8 events per k-block in CTAs 0/1
+and prints steady-state intervals: who waits on whom."""
+import ctypes
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from bench import Problem  # noqa: E402
+from paper_2508_16584_b200 import _lib  # noqa: E402
+
+L = ctypes.CDLL(str(_lib.PKG / "libtagg_trace.so"))
+for name, (res, args) in _lib.SIGNATURES.items():
+    fn = getattr(L, name)
+    fn.restype, fn.argtypes = res, args
+
+EV = ["mma_tempty", "mma_full", "mma_issued", "prod_empty", "promo_full", "promo_freed", "promo_done", "promo2_full"]
+dev = torch.device("cuda", 0)
+buf = torch.zeros((2, 8, 1024), dtype=torch.int64, device=dev)
+
+
+def run(P, flags, G):
+    rc = L.tagg_grouped_gemm_fp8(P.a.data_ptr(), P.a.stride(0), P.sa.data_ptr(), P.m_alloc, P.b.data_ptr(), 0, G,
+                                 P.sb.data_ptr(), P.sb.stride(0), P.sb.stride(1), P.sb.stride(2), P.gs[0].data_ptr(),
+                                 G, P.n, P.k, P.out.data_ptr(), P.n, P.m_alloc, None, None, flags,
+                                 torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, rc
+
+
+def report(tr, lo, hi, label):
+    t = tr[0].astype(np.float64)  # CTA 0 (leader)
+    d = lambda a, b, sh=0: (t[EV.index(a), lo:hi] - t[EV.index(b), lo - sh:hi - sh])  # noqa: E731
+    rows = {
+        "mma issue period": d("mma_issued", "mma_issued", 1),
+        "mma wait tempty (after prev issue)": d("mma_tempty", "mma_issued", 1),
+        "mma wait full": d("mma_full", "mma_tempty"),
+        "mma issue->promo sees full": d("promo_full", "mma_issued"),
+        "promo wait full (after prev done)": d("promo_full", "promo_done", 1),
+        "promo full->freed (drain)": d("promo_freed", "promo_full"),
+        "promo freed->done (math tail)": d("promo_done", "promo_freed"),
+        "promo freed(i-2)->mma tempty(i)": d("mma_tempty", "promo_freed", 2),
+        "prod empty period": d("prod_empty", "prod_empty", 1),
+    }
+    print(f"--- {label}: k-block iterations [{lo},{hi}) of CTA 0, clk (median / p10 / p90)")
+    for k, v in rows.items():
+        print(f"  {k:38s} {np.median(v):8.0f} {np.percentile(v, 10):8.0f} {np.percentile(v, 90):8.0f}")
+    t1 = tr[1].astype(np.float64)
+    v = t1[EV.index("promo_full"), lo:hi] - t1[EV.index("promo_full"), lo - 1:hi - 1]
+    print(f"  {'CTA1 promo full period':38s} {np.median(v):8.0f}")
+
+
+cases = [("sq8192", [(8192,)], 8192, 8192, 1), ("sweep_r64", [tuple(128 * g + 64 for g in range(8))], 4096, 7168, 8)]
+if len(sys.argv) > 1 and sys.argv[1] == "longk":
+    # one pair tile per cluster, 256 k-blocks per tile: no tile transitions in the window
+    cases = [("longk", [(256 * 74,)], 256, 8192, 1)]
+for name, sizes, n, k, G in cases:
+    P = Problem(torch, name, sizes, n, k, G, dev, seed=1)
+    for label, flags in [("full", 16), ("nomath", 16 | 1024), ("noprom", 16 | 512), ("neither", 16 | 256 | 512),
+                         ("noload", 16 | 256), ("sbconst", 16 | 65536), ("sbconst_saflat", 16 | 65536 | 2048),
+                         ("sbconst_neither", 16 | 65536 | 256 | 512)]:
+        L.tagg_debug_trace(None)
+        run(P, flags, G)
+        L.tagg_debug_trace(ctypes.c_void_p(buf.data_ptr()))
+        buf.zero_()
+        run(P, flags, G)
+        torch.cuda.synchronize()
+        L.tagg_debug_trace(None)
+        report(buf.cpu().numpy(), 8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60}[name], f"{name} {label}")
+    del P
