@@ -65,6 +65,9 @@ constexpr uint32_t kStageBytesA = BM * BK;   // 128 rows x 128 K
 constexpr uint32_t kChunkBytesC = BM * 128;  // 128 rows x 64 bf16 columns
 constexpr uint32_t kCStagingBytes = 2 * kChunkBytesC;
 constexpr int kPoolSize = 8;  // heights 1, 2, ..., 128 (descriptors.py:31-35)
+constexpr int kSbCols = 2;                    // S_B column blocks a CTA's tile can touch (256 columns)
+constexpr int kMaxKb = 128;                   // K <= 16384 (S_B staging below)
+constexpr uint32_t kSbBufBytes = kSbCols * kMaxKb * 4;
 constexpr uint32_t kDbgNoLoad = 1u << 8;     // diagnostics: producer signals stages without loads
 constexpr uint32_t kDbgNoPromote = 1u << 9;  // diagnostics: promotion skips tcgen05.ld + math
 constexpr uint32_t kDbgNoMath = 1u << 10;    // diagnostics: promotion drains TMEM but skips the FFMA math
@@ -83,7 +86,7 @@ struct Params {
   int64_t sb_sg, sb_skb, sb_snb;
   int32_t G, N, K, kb_count, n_tiles, sa_rb, b_kmajor, b_shared;
   uint32_t stages, sa_buf_bytes;
-  uint32_t off_a, off_b, off_c, off_sa, off_tab, off_bar;
+  uint32_t off_a, off_b, off_c, off_sa, off_sb, off_tab, off_bar;
   uint32_t dbg;
 };
 
@@ -170,11 +173,17 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   const bool is_leader = rank == 0;
   const int cluster_id = blockIdx.x / kCG;
   const int num_clusters = gridDim.x / kCG;
+#ifdef TAGG_TRACE
+  const uint32_t dbg = p.dbg;  // ablation switches exist only in the diagnostics build
+#else
+  constexpr uint32_t dbg = 0;
+#endif
 
   uint8_t* sA = smem + p.off_a;
   uint8_t* sB = smem + p.off_b;
   uint8_t* sC = smem + p.off_c;
   uint8_t* sSA = smem + p.off_sa;
+  uint8_t* sSB = smem + p.off_sb;  // [2 buffers][kSbCols][kbc] fp32: this tile's S_B columns
   int32_t* tab_tile = reinterpret_cast<int32_t*>(smem + p.off_tab);  // [G+1]
   int32_t* tab_row = tab_tile + (G + 1);                                // [G+1]
   int32_t* tab_size = tab_row + (G + 1);                                // [G]
@@ -201,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       mbar_init(&tempty[i], kNumPromoWarps * kCG);     // promotion warps of every CTA in the pair
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&safull[i], 1);
+      mbar_init(&safull[i], 1 + 32);  // S_A bulk copy (expect_tx) + 32 producer lanes' S_B cp.async
       mbar_init(&saempty[i], kNumPromoWarps);
     }
     fence_mbar_init();
@@ -238,23 +247,43 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   tc_fence_before();
   if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int total_tiles = tab_tile[G];
+  // Values needed after the setmaxnreg split are re-read inside each role (ld.shared is
+  // cheap); keeping them live across it makes ptxas spill them into the hot loops.
   const int kbc = p.kb_count;
   const int rb = p.sa_rb;
 
   if (warp < kFirstPromoWarp) {
    setmaxnreg_dec<kRegsControl>();
+   const int total_tiles = ld_shared_s32(smem_u32(&tab_tile[G]));
    if (warp == 0) {
     // ========================================================== TMA producer
+    // Per tile: the S_A over-fetch window (one 1-D bulk copy by lane 0) and this tile's
+    // S_B columns (4-byte cp.async by all 32 lanes, tracked by the same barrier), then
+    // the A / B k-blocks (lane 0).
     uint32_t stage = 0, phase = 0, sab = 0, saph = 0, kiter = 0;
-    const bool elected = elect_one();
+    const uint32_t sfull0 = smem_u32(&safull[0]), sempty0 = smem_u32(&saempty[0]);
+    const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB), sSA0 = smem_u32(sSA), sSB0 = smem_u32(sSB);
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int gb = p.b_shared ? 0 : T.g;
-      // ---- S_A over-fetch window (one 1-D bulk copy per tile, own rows)
-      mbar_wait(&saempty[sab], saph ^ 1);
-      if (elected) {
+      mbar_wait_addr(sempty0 + 8 * sab, saph ^ 1);
+      // ---- S_B columns of the tile (engine.py:166-169: column block n // 128)
+      {
+        const float* sbg = p.sb + static_cast<int64_t>(gb) * p.sb_sg;
+        const uint32_t dst0 = sSB0 + sab * kSbBufBytes;
+#pragma unroll
+        for (int c = 0; c < kSbCols; ++c) {
+          const int nb = (T.n0 >> 7) + c;
+          if (T.n0 + 128 * c >= p.N) break;
+          for (int kb = lane; kb < kbc; kb += 32)
+            cp_async_4(dst0 + 4u * (c * kbc + kb), sbg + static_cast<int64_t>(kb) * p.sb_skb +
+                                                       static_cast<int64_t>(nb) * p.sb_snb);
+        }
+        cp_async_mbar_arrive_noinc(sfull0 + 8 * sab);
+      }
+      // ---- S_A over-fetch window (prefetch.py:50-72)
+      if (lane == 0) {
         const int rp = sa_row_prev(T.row0, rb);
         const int64_t start_row = static_cast<int64_t>(T.row0) - rp;
         const int64_t want = ((static_cast<int64_t>(rp + BM) * rb) + 15) & ~int64_t(15);
@@ -267,47 +296,45 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         const uint8_t* src = reinterpret_cast<const uint8_t*>(p.sa) + start_row * rb;
         for (uint32_t i = 0; i < tail; i += 4)  // < 16 B at the very end of S_A
           *reinterpret_cast<float*>(dst + bulk + i) = __ldg(reinterpret_cast<const float*>(src + bulk + i));
-        mbar_arrive_expect_tx(&safull[sab], bulk);
-        if (bulk) bulk_load_1d(dst, src, bulk, &safull[sab]);
+        mbar_arrive_expect_tx_addr(sfull0 + 8 * sab, bulk);
+        if (bulk) bulk_load_1d_addr(sSA0 + sab * p.sa_buf_bytes, src, bulk, sfull0 + 8 * sab);
       }
-      __syncwarp();
       if (++sab == 2) { sab = 0; saph ^= 1; }
-      // ---- A / B k-blocks.  This CTA stages its 128 rows of A and its
-      // 128-column share of B; completion is counted on the leader's barrier.
-      const int nb = T.n0 + rank * C::kBCols;
-      for (int kb = 0; kb < kbc; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) trace_stamp(p.trace, kEvProdEmpty, kiter);  // no-op unless TAGG_TRACE
-        ++kiter;
-        if (elected) {
-          if (p.dbg & kDbgNoLoad) {
-            if (is_leader) mbar_arrive(&full[stage]);
+      // ---- A / B k-blocks.  This CTA stages its 128 rows of A and its B column share;
+      // completion is counted on the leader's barrier.
+      if (lane == 0) {
+        const int nb = T.n0 + rank * C::kBCols;
+        for (int kb = 0; kb < kbc; ++kb) {
+          mbar_wait_addr(empty0 + 8 * stage, phase ^ 1);
+          trace_stamp(p.trace, kEvProdEmpty, kiter++);
+          const uint32_t fb = full0 + 8 * stage;
+          if (dbg & kDbgNoLoad) {
+            if (is_leader) mbar_arrive_addr(fb);
           } else {
-            if (is_leader) mbar_arrive_expect_tx(&full[stage], C::kStageTx);
+            if (is_leader) mbar_arrive_expect_tx_addr(fb, C::kStageTx);
             const int cb0 = p.b_kmajor ? kb * BK : nb;
             const int cb1 = p.b_kmajor ? nb : kb * BK;
-            if constexpr (kCG == 1) {
-              tma_load_2d(&p.tmap_a, &full[stage], sA + stage * kStageBytesA, kb * BK, T.row0);
-              tma_load_3d(&p.tmap_b, &full[stage], sB + stage * C::kStageBytesB, cb0, cb1, gb);
-            } else {
-              tma_load_2d_cg2(&p.tmap_a, &full[stage], sA + stage * kStageBytesA, kb * BK, T.row0);
-              tma_load_3d_cg2(&p.tmap_b, &full[stage], sB + stage * C::kStageBytesB, cb0, cb1, gb);
-            }
+            tma_load_2d_u32<kCG>(&p.tmap_a, fb, sA0 + stage * kStageBytesA, kb * BK, T.row0);
+            tma_load_3d_u32<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb);
           }
+          if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == S) { stage = 0; phase ^= 1; }
       }
+      __syncwarp();
     }
     // Producer tail: wait until every issued stage has been consumed, so no MMA
     // commit can still target this CTA's barriers after it exits.
-    for (uint32_t i = 0; i < S; ++i) {
-      mbar_wait(&empty[stage], phase ^ 1);
-      if (++stage == S) { stage = 0; phase ^= 1; }
+    if (lane == 0) {
+      for (uint32_t i = 0; i < S; ++i) {
+        mbar_wait_addr(empty0 + 8 * stage, phase ^ 1);
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
     }
+    __syncwarp();
   } else if (warp == 1) {
-    // ========================================================== MMA issuer (leader CTA)
-    if (is_leader) {
+    // ========================================================== MMA issuer (leader CTA, one thread)
+    if (is_leader && lane == 0) {
+      const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
       const uint32_t idesc = idesc_e4m3_f32(BM * kCG, C::kBN, p.b_kmajor == 0);
       const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), 16, 1024);
       // B: K-major rows are 128 B (SWIZZLE_128B, 8-row groups of 1 KB).  MN-major rows
@@ -318,38 +345,37 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
                      : (C::kBCols == 128 ? umma_desc_sw128(smem_u32(sB), C::kStageBytesB, 1024)
                                          : umma_desc_sw64(smem_u32(sB), C::kStageBytesB, 512));
       const uint32_t b_kstep = p.b_kmajor ? (32u >> 4) : ((32u * C::kBCols) >> 4);  // desc units per K=32
-      const bool elected = elect_one();
+      const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+      const uint32_t tfull0 = smem_u32(&tfull[0]), tempty0 = smem_u32(&tempty[0]);
       uint32_t stage = 0, phase = 0, acc = 0, accph = 0, kiter = 0;
-      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
-        for (int kb = 0; kb < kbc; ++kb) {
-          mbar_wait(&tempty[acc], accph ^ 1);
-          if (lane == 0) trace_stamp(p.trace, kEvMmaTempty, kiter);
-          mbar_wait(&full[stage], phase);
-          if (lane == 0) trace_stamp(p.trace, kEvMmaFull, kiter);
-          tc_fence_after();
-          if (elected) {
-            const uint64_t ad = a_desc0 + ((stage * kStageBytesA) >> 4);
-            const uint64_t bd = b_desc0 + ((stage * C::kStageBytesB) >> 4);
-            const uint32_t d_tmem = tmem_base + acc * C::kBN;
+      const int my_kblocks = ((total_tiles - cluster_id + num_clusters - 1) / num_clusters) * kbc;
+      for (int i = 0; i < my_kblocks; ++i) {
+        mbar_wait_addr(tempty0 + 8 * acc, accph ^ 1);
+        trace_stamp(p.trace, kEvMmaTempty, kiter);
+        mbar_wait_addr(full0 + 8 * stage, phase);
+        trace_stamp(p.trace, kEvMmaFull, kiter);
+        tc_fence_after();
+        const uint64_t ad = a_desc0 + ((stage * kStageBytesA) >> 4);
+        const uint64_t bd = b_desc0 + ((stage * C::kStageBytesB) >> 4);
+        const uint32_t d_tmem = tmem_base + acc * C::kBN;
 #pragma unroll
-            for (int k = 0; k < BK / 32; ++k)
-              mma_f8f6f4<kCG>(d_tmem, ad + static_cast<uint64_t>(k * (32 >> 4)),
-                              bd + static_cast<uint64_t>(k * b_kstep), idesc, k > 0 ? 1u : 0u);
-            mma_commit<kCG>(&empty[stage]);  // smem slot free (both CTAs) once these MMAs retire
-            mma_commit<kCG>(&tfull[acc]);    // k-block partial ready for promotion (both CTAs)
-          }
-          __syncwarp();
-          if (lane == 0) trace_stamp(p.trace, kEvMmaIssued, kiter);
-          ++kiter;
-          if (++stage == S) { stage = 0; phase ^= 1; }
-          if (++acc == C::kNumAcc) { acc = 0; accph ^= 1; }
-        }
+        for (int k = 0; k < BK / 32; ++k)
+          mma_f8f6f4<kCG>(d_tmem, ad + static_cast<uint64_t>(k * (32 >> 4)), bd + static_cast<uint64_t>(k * b_kstep),
+                          idesc, k > 0 ? 1u : 0u);
+        mma_commit_addr<kCG>(empty0 + 8 * stage);  // smem slot free (both CTAs) once these MMAs retire
+        mma_commit_addr<kCG>(tfull0 + 8 * acc);    // k-block partial ready for promotion (both CTAs)
+        trace_stamp(p.trace, kEvMmaIssued, kiter++);
+        if (++stage == S) { stage = 0; phase ^= 1; }
+        if (++acc == C::kNumAcc) { acc = 0; accph ^= 1; }
       }
     }
+    __syncwarp();
    }
   } else {
     setmaxnreg_inc<kRegsPromo>();
     // ========================================================== promotion + epilogue
+    const int total_tiles = ld_shared_s32(smem_u32(&tab_tile[G]));
+    const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
     constexpr int kCPT = C::kColsPerThread;  // 64 or 128
     const int pw = warp - kFirstPromoWarp;
     const int q = warp & 3;          // TMEM lane quarter this warp may access
@@ -357,8 +383,11 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const int r = 32 * q + lane;     // tile row owned by this thread
     const int ptid = threadIdx.x - 32 * kFirstPromoWarp;
     const uint32_t t_lane = static_cast<uint32_t>(32 * q) << 16;
-    const bool no_promote = (p.dbg & kDbgNoPromote) != 0;
-    const bool no_math = (p.dbg & kDbgNoMath) != 0;
+    // this thread's S_B column block within the tile (kCPT columns never straddle a 128-block)
+    const int sb_col = (half * kCPT) >> 7;
+    const uint32_t tfull0 = smem_u32(&tfull[0]), tempty0 = smem_u32(&tempty[0]);
+    const uint32_t sfull0 = smem_u32(&safull[0]), sempty0 = smem_u32(&saempty[0]);
+    const uint32_t sSA0 = smem_u32(sSA), sSB0 = smem_u32(sSB);
     uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0;
 #ifdef TAGG_TRACE
     const bool tr_a = p.trace != nullptr && pw == 0 && lane == 0;
@@ -369,30 +398,29 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int rp = sa_row_prev(T.row0, rb);
-      const float* sbp = p.sb + (p.b_shared ? 0 : static_cast<int64_t>(T.g) * p.sb_sg) +
-                         static_cast<int64_t>((T.n0 + half * kCPT) >> 7) * p.sb_snb;
-      const int64_t sb_step = p.sb_skb;
-      mbar_wait(&safull[sab], saph);
-      // this thread's S_A row in the over-fetched window
-      const uint32_t sa_row = smem_u32(sSA) + sab * p.sa_buf_bytes + static_cast<uint32_t>(rp + r) * rb;
+      mbar_wait_addr(sfull0 + 8 * sab, saph);
+      // this thread's S_A row in the over-fetched window and its S_B column, both in smem
+      const uint32_t sa_row = sSA0 + sab * p.sa_buf_bytes + static_cast<uint32_t>(rp + r) * rb;
+      const uint32_t sb_colp = sSB0 + sab * kSbBufBytes + 4u * static_cast<uint32_t>(sb_col * kbc);
       float acc[kCPT];
 #pragma unroll
       for (int i = 0; i < kCPT; ++i) acc[i] = 0.0f;
-      float sb_next = __ldg(sbp);
+      // s = fl(sa * sb) (engine.py:161-164), computed one k-block ahead
+      float s_next = __fmul_rn(ld_shared_f32(sa_row), ld_shared_f32(sb_colp));
       for (int kb = 0; kb < kbc; ++kb) {
-        const float sbv = sb_next;
-        sbp += sb_step;
-        if (kb + 1 < kbc) sb_next = __ldg(sbp);
-        const float s = __fmul_rn(ld_shared_f32(sa_row + 4u * kb), sbv);
-        mbar_wait(&tfull[acc_i], accph);
+        const float s = s_next;
+        if (kb + 1 < kbc)
+          s_next = __fmul_rn(ld_shared_f32(sa_row + 4u * (kb + 1)), ld_shared_f32(sb_colp + 4u * (kb + 1)));
+        mbar_wait_addr(tfull0 + 8 * acc_i, accph);
         if (tr_a) trace_stamp(p.trace, kEvPromoFull, kiter);
         if (tr_b) trace_stamp(p.trace, kEvPromo2Full, kiter);
         tc_fence_after();
-        if (no_promote) {
+        const uint32_t tempty_b = tempty0 + 8 * acc_i;
+        if (dbg & kDbgNoPromote) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            if constexpr (kCG == 1) mbar_arrive(&tempty[acc_i]); else mbar_arrive_leader(&tempty[acc_i]);
+            if constexpr (kCG == 1) mbar_arrive_addr(tempty_b); else mbar_arrive_leader_addr(tempty_b);
           }
           if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
           ++kiter;
@@ -400,45 +428,40 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           continue;
         }
         const uint32_t taddr = tmem_base + t_lane + acc_i * C::kBN + half * kCPT;
-        // Software-pipelined TMEM drain: chunk c+1 is in flight while chunk c is
-        // promoted; the buffer is handed back as soon as the last chunk has landed.
+        // TMEM drain, 32 columns at a time; the buffer is handed back as soon as the
+        // last chunk has landed in registers.
         constexpr int kChunks = kCPT / 32;
-        uint32_t va[32], vb[32];
-        tmem_ld_32x32b_x32(taddr, va);
-        tmem_wait_ld_dep(va);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
-          uint32_t(&cur)[32] = (c & 1) ? vb : va;
-          uint32_t(&nxt)[32] = (c & 1) ? va : vb;
-          if (c + 1 < kChunks) {
-            tmem_ld_32x32b_x32(taddr + 32 * (c + 1), nxt);
-          } else {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(taddr + 32 * c, v);
+          tmem_wait_ld_dep(v);
+          if (c + 1 == kChunks) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-              if constexpr (kCG == 1) mbar_arrive(&tempty[acc_i]); else mbar_arrive_leader(&tempty[acc_i]);
+              if constexpr (kCG == 1) mbar_arrive_addr(tempty_b); else mbar_arrive_leader_addr(tempty_b);
             }
             if (tr_a) trace_stamp(p.trace, kEvPromoFreed, kiter);
           }
-          if (no_math) {
-            acc[32 * c] += __uint_as_float(cur[c]);
+          if (dbg & kDbgNoMath) {
+            acc[32 * c] += __uint_as_float(v[c]);
           } else if constexpr (kExact) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              acc[32 * c + i] = __fadd_rn(acc[32 * c + i], __fmul_rn(__uint_as_float(cur[i]), s));
+              acc[32 * c + i] = __fadd_rn(acc[32 * c + i], __fmul_rn(__uint_as_float(v[i]), s));
           } else {
 #pragma unroll
             for (int i = 0; i < 32; i += 2)
-              ffma2(acc[32 * c + i], acc[32 * c + i + 1], __uint_as_float(cur[i]), __uint_as_float(cur[i + 1]), s);
+              ffma2(acc[32 * c + i], acc[32 * c + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]), s);
           }
-          if (c + 1 < kChunks) tmem_wait_ld_dep(nxt);
         }
         if (tr_a) trace_stamp(p.trace, kEvPromoDone, kiter);
         ++kiter;
         if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&saempty[sab]);
+      if (lane == 0) mbar_arrive_addr(sempty0 + 8 * sab);
       if (++sab == 2) { sab = 0; saph ^= 1; }
 
       // ---- epilogue: bf16 -> swizzled smem staging (2 chunks of 64 columns)
@@ -513,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<kCG>(tmem_base, kTmemCols);
+    tmem_dealloc<kCG>(ld_shared_u32(smem_u32(tmem_slot)), kTmemCols);
   }
 }
 
@@ -638,7 +661,8 @@ static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_a
   p.off_b = stages * kStageBytesA;
   p.off_c = p.off_b + stages * stage_bytes_b;
   p.off_sa = p.off_c + kCStagingBytes;
-  p.off_tab = p.off_sa + 2 * sa_buf;
+  p.off_sb = p.off_sa + 2 * sa_buf;
+  p.off_tab = p.off_sb + 2 * kSbBufBytes;
   const uint32_t tab_bytes = align_up(4u * static_cast<uint32_t>(2 * (G + 1) + 2 * G), 16);
   p.off_bar = p.off_tab + tab_bytes;
   const uint32_t bar_bytes = (2 * stages + 2 * num_acc + 4) * 8 + 16;
@@ -735,6 +759,7 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   const int num_acc = 512 / bn;
   const uint32_t stage_bytes_b = static_cast<uint32_t>(BK * (bn / cg));
   const int kb_count = (K + BK - 1) / BK;
+  if (kb_count > kMaxKb) return TAGG_ERR_UNSUPPORTED;  // S_B staging holds 128 k-blocks (K <= 16384)
   const int rb = 4 * kb_count;
   Params p;
   std::memset(&p, 0, sizeof(p));

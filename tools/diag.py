@@ -3,7 +3,14 @@ import sys, json
 sys.path.insert(0, ".")
 import torch
 import paper_2508_16584_b200 as tg
-from paper_2508_16584_b200._lib import lib
+import ctypes
+from paper_2508_16584_b200 import _lib
+
+# the ablation flags are honoured only by the diagnostics build (make -C paper_2508_16584_b200/csrc trace)
+_L = ctypes.CDLL(str(_lib.PKG / "libtagg_trace.so"))
+for _n, (_r, _a) in _lib.SIGNATURES.items():
+    getattr(_L, _n).restype, getattr(_L, _n).argtypes = _r, _a
+lib = lambda: _L  # noqa: E731
 from bench import Problem
 
 dev = torch.device("cuda", 0)
@@ -12,8 +19,9 @@ for name, sizes, n, k, G in [("sweep_r64", [tuple(128 * g + 64 for g in range(8)
                              ("sq8192", [(8192,)], 8192, 8192, 1)]:
     P = Problem(torch, name, sizes, n, k, G, dev, seed=1)
     variants = [("n256", 16), ("n256_nomath", 16 | 1024), ("n256_noprom", 16 | 512), ("n256_neither", 16 | 256 | 512),
-                ("n256_noload", 16 | 256), ("n256_noload_nomath", 16 | 256 | 1024), ("n256_exact", 16 | 1)]
-    for label, flags in variants + variants[:4]:  # second pass: compare against clock drift
+                ("n128", 8), ("n128_nomath", 8 | 1024), ("n128_noprom", 8 | 512), ("n128_neither", 8 | 256 | 512),
+                ("c1_128", 4), ("c1_128_noprom", 4 | 512), ("c1_128_neither", 4 | 256 | 512)]
+    for label, flags in variants:
         def run():
             rc = lib().tagg_grouped_gemm_fp8(P.a.data_ptr(), P.a.stride(0), P.sa.data_ptr(), P.m_alloc,
                                              P.b.data_ptr(), 0, G, P.sb.data_ptr(), P.sb.stride(0), P.sb.stride(1),
