@@ -261,9 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     // S_B columns (4-byte cp.async by all 32 lanes, tracked by the same barrier), then
     // the A / B k-blocks (lane 0).
     uint32_t stage = 0, phase = 0, sab = 0, saph = 0, kiter = 0;
-    const uint32_t sfull0 = smem_u32(&safull[0]), sempty0 = smem_u32(&saempty[0]);
-    const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
-    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB), sSA0 = smem_u32(sSA), sSB0 = smem_u32(sSB);
+    const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
+    const uint32_t full0 = opaque_u32(smem_u32(&full[0])), empty0 = opaque_u32(smem_u32(&empty[0]));
+    const uint32_t sA0 = opaque_u32(smem_u32(sA)), sB0 = opaque_u32(smem_u32(sB));
+    const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int gb = p.b_shared ? 0 : T.g;
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   } else if (warp == 1) {
     // ========================================================== MMA issuer (leader CTA, one thread)
     if (is_leader && lane == 0) {
-      const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
+      const uint32_t tmem_base = opaque_u32(ld_shared_u32(smem_u32(tmem_slot)));
       const uint32_t idesc = idesc_e4m3_f32(BM * kCG, C::kBN, p.b_kmajor == 0);
       const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), 16, 1024);
       // B: K-major rows are 128 B (SWIZZLE_128B, 8-row groups of 1 KB).  MN-major rows
@@ -345,8 +346,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
                      : (C::kBCols == 128 ? umma_desc_sw128(smem_u32(sB), C::kStageBytesB, 1024)
                                          : umma_desc_sw64(smem_u32(sB), C::kStageBytesB, 512));
       const uint32_t b_kstep = p.b_kmajor ? (32u >> 4) : ((32u * C::kBCols) >> 4);  // desc units per K=32
-      const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
-      const uint32_t tfull0 = smem_u32(&tfull[0]), tempty0 = smem_u32(&tempty[0]);
+      const uint32_t full0 = opaque_u32(smem_u32(&full[0])), empty0 = opaque_u32(smem_u32(&empty[0]));
+      const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
       uint32_t stage = 0, phase = 0, acc = 0, accph = 0, kiter = 0;
       const int my_kblocks = ((total_tiles - cluster_id + num_clusters - 1) / num_clusters) * kbc;
       for (int i = 0; i < my_kblocks; ++i) {
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     setmaxnreg_inc<kRegsPromo>();
     // ========================================================== promotion + epilogue
     const int total_tiles = ld_shared_s32(smem_u32(&tab_tile[G]));
-    const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
+    const uint32_t tmem_base = opaque_u32(ld_shared_u32(smem_u32(tmem_slot)));
     constexpr int kCPT = C::kColsPerThread;  // 64 or 128
     const int pw = warp - kFirstPromoWarp;
     const int q = warp & 3;          // TMEM lane quarter this warp may access
@@ -385,9 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t t_lane = static_cast<uint32_t>(32 * q) << 16;
     // this thread's S_B column block within the tile (kCPT columns never straddle a 128-block)
     const int sb_col = (half * kCPT) >> 7;
-    const uint32_t tfull0 = smem_u32(&tfull[0]), tempty0 = smem_u32(&tempty[0]);
-    const uint32_t sfull0 = smem_u32(&safull[0]), sempty0 = smem_u32(&saempty[0]);
-    const uint32_t sSA0 = smem_u32(sSA), sSB0 = smem_u32(sSB);
+    const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
+    const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
+    const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
     uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0;
 #ifdef TAGG_TRACE
     const bool tr_a = p.trace != nullptr && pw == 0 && lane == 0;

@@ -15,6 +15,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// An opaque copy: ptxas cannot rematerialise the value (it re-derived shared-window
+// addresses with S2R/S2UR + constant loads inside the hot loops, right on the
+// barrier wait / arrive critical path).
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 // ---------------------------------------------------------------- mbarrier
 // Bounded spin: a protocol bug traps (error 719) instead of hanging the GPU.
 #ifndef TAGG_WAIT_LIMIT

@@ -24,6 +24,7 @@ def load(path):
     return L
 dev = torch.device("cuda", 0)
 shapes = [
+    ("tiles4", [(256 * 74,)], 1024, 8192, 1, "kn"),
     ("sq8192", [(8192,)], 8192, 8192, 1, "kn"),
     ("sweep_r64", [tuple(128 * g + 64 for g in range(8))], 4096, 7168, 8, "kn"),
     ("ds_gateup", [tuple(int(x) for x in deepseek_gateup_sizes(0)[1])], 4096, 7168, 32, "kn"),

@@ -58,8 +58,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "longk":
 for name, sizes, n, k, G in cases:
     P = Problem(torch, name, sizes, n, k, G, dev, seed=1)
     for label, flags in [("full", 16), ("nomath", 16 | 1024), ("noprom", 16 | 512), ("neither", 16 | 256 | 512),
-                         ("noload", 16 | 256), ("sbconst", 16 | 65536), ("sbconst_saflat", 16 | 65536 | 2048),
-                         ("sbconst_neither", 16 | 65536 | 256 | 512)]:
+                         ("noload", 16 | 256)]:
         L.tagg_debug_trace(None)
         run(P, flags, G)
         L.tagg_debug_trace(ctypes.c_void_p(buf.data_ptr()))
