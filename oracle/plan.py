@@ -67,6 +67,49 @@ def format_plan(plans) -> str:
     return "\n".join(lines)
 
 
+def kernel_tile_map(group_sizes, n: int, tile: str = "pair_n256", c_row_offsets=None):
+    """The store geometry the B200 kernel uses, stated with the reference planner.
+
+    Every stored piece follows plan_two_phase (descriptors.py:72-106) for its block
+    height.  For the 1-CTA and 256x128 pair tiles that is exactly the reference tile
+    loop (tile_map, block_m = 128).  The default 256x256 pair tile computes a group's
+    last pair tile with at most 128 valid rows as a HALF tile (one tcgen05.mma M=128
+    per K step, 64 rows per CTA), and each CTA stores its 64-row piece with the
+    reference plan at block_rows = 64: a full piece is one 64-row store, a residual
+    piece the two-phase store.  The mapping of rows to groups (which C rows each
+    piece writes, never a row past M_g) is the reference's in every case.
+    Records: (g, m_tile, n0, a_row0, valid, d, phaseA_gmem_row, phaseB_smem_row,
+    phaseB_gmem_row), m_tile = the reference's 128-row tile index.
+    """
+    if tile != "pair_n256":
+        return tile_map(group_sizes, n, c_row_offsets=c_row_offsets)
+    recs = []
+    off = 0
+    for g, rows in enumerate(group_sizes):
+        rows = int(rows)
+        coff = off if c_row_offsets is None else int(c_row_offsets[g])
+        for pm in range(-(-rows // 256)):
+            base = 256 * pm
+            if rows - base <= 128:  # half tile: two 64-row pieces
+                for j in range(2):
+                    r0 = base + 64 * j
+                    v = min(64, rows - r0)
+                    if v <= 0:
+                        continue
+                    d = 1 << (v.bit_length() - 1)
+                    for n0 in range(0, n, 128):
+                        recs.append((g, 2 * pm, n0, off + r0, v, d, coff + r0, v - d, coff + r0 + v - d))
+            else:
+                for t in (2 * pm, 2 * pm + 1):
+                    r0 = 128 * t
+                    v = min(128, rows - r0)
+                    d = 1 << (v.bit_length() - 1)
+                    for n0 in range(0, n, 128):
+                        recs.append((g, t, n0, off + r0, v, d, coff + r0, v - d, coff + r0 + v - d))
+        off += rows
+    return recs
+
+
 def scale_row_bytes(k: int) -> int:
     """prefetch.py:22-24"""
     return 4 * (-(-k // 128))

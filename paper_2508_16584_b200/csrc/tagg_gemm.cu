@@ -98,6 +98,7 @@ struct Cfg {
   static constexpr uint32_t kStageBytesB = BK * kBCols;
   static constexpr int kNumAcc = 512 / kBN;          // TMEM accumulation buffers
   static constexpr int kColsPerThread = kBN / 2;     // two warps per TMEM lane quarter
+  static constexpr bool kHalfTiles = (kCG == 2 && kBN == 256);
   static constexpr uint32_t kStageTx = kCG * (kStageBytesA + kStageBytesB);  // bytes landing per stage
   static_assert(kBCols == 64 || kBCols == 128, "B share per CTA must be 64 or 128 columns");
 };
@@ -117,11 +118,16 @@ __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int ev, uint
 
 struct Tile {
   int g, mt, n0, row0, valid, crow0;
+  bool half;  // pair tile with <= 128 valid rows: M=128 MMA, 64 rows per CTA
 };
 
-// Scheduled tile t -> this CTA's 128-row slice.  A scheduled tile covers
-// kTileM rows (pair index pm) x kBN columns of group g; CTA `rank` owns rows
-// [pm*kTileM + 128*rank, +128).  valid <= 0 when the slice lies past M_g.
+// Scheduled tile t -> this CTA's row slice.  A scheduled tile covers kTileM rows
+// (pair index pm) x kBN columns of group g; CTA `rank` owns rows
+// [pm*kTileM + 128*rank, +128) (mt = the reference's 128-row tile index).  A pair
+// tile at the end of a group with at most 128 valid rows is a HALF tile (256-column
+// pair tiles only): one tcgen05.mma M=128 cta_group::2 per K step computes its
+// 128 rows as 64 per CTA, rows [pm*256 + 64*rank, +64), so no MMA work is spent
+// on the pair's empty second half.  valid <= 0 when the slice lies past M_g.
 template <int kCG, int kBN>
 __device__ __forceinline__ Tile decode_tile(int t, int rank, const int32_t* tab_tile, const int32_t* tab_row,
                                             const int32_t* tab_size, const int32_t* tab_crow, int G) {
@@ -143,11 +149,20 @@ __device__ __forceinline__ Tile decode_tile(int t, int rank, const int32_t* tab_
   const int h = min(kRasterM, ptiles - sr * kRasterM);
   const int local = l - sr * kRasterM * ntiles;
   const int pm = sr * kRasterM + local % h;
-  T.mt = pm * kCG + rank;
   T.n0 = (local / h) * Cfg<kCG, kBN>::kBN;
-  T.row0 = tab_row[lo] + T.mt * BM;
-  T.valid = min(BM, m - T.mt * BM);
-  T.crow0 = tab_crow[lo] + T.mt * BM;
+  T.half = Cfg<kCG, kBN>::kHalfTiles && (m - pm * Cfg<kCG, kBN>::kTileM) <= BM;
+  if (T.half) {
+    T.mt = pm * kCG;
+    const int r0 = pm * Cfg<kCG, kBN>::kTileM + (BM / 2) * rank;
+    T.row0 = tab_row[lo] + r0;
+    T.valid = min(BM / 2, m - r0);
+    T.crow0 = tab_crow[lo] + r0;
+  } else {
+    T.mt = pm * kCG + rank;
+    T.row0 = tab_row[lo] + T.mt * BM;
+    T.valid = min(BM, m - T.mt * BM);
+    T.crow0 = tab_crow[lo] + T.mt * BM;
+  }
   return T;
 }
 
@@ -333,10 +348,14 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ========================================================== MMA issuer (leader CTA, one thread)
-    if (is_leader && lane == 0) {
-      const uint32_t tmem_base = opaque_u32(ld_shared_u32(smem_u32(tmem_slot)));
+    // ========================================================== MMA issuer (leader CTA)
+    // The whole warp runs the loop (every value stays warp-uniform, in uniform
+    // registers); one elected lane issues the MMAs and commits.
+    if (is_leader) {
+      const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
       const uint32_t idesc = idesc_e4m3_f32(BM * kCG, C::kBN, p.b_kmajor == 0);
+      // half tiles (M=128): the instruction descriptor's M field
+      const uint32_t idesc_half = idesc_e4m3_f32(BM * kCG / 2, C::kBN, p.b_kmajor == 0);
       const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), 16, 1024);
       // B: K-major rows are 128 B (SWIZZLE_128B, 8-row groups of 1 KB).  MN-major rows
       // hold this CTA's kBCols columns: 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B,
@@ -346,28 +365,37 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
                      : (C::kBCols == 128 ? umma_desc_sw128(smem_u32(sB), C::kStageBytesB, 1024)
                                          : umma_desc_sw64(smem_u32(sB), C::kStageBytesB, 512));
       const uint32_t b_kstep = p.b_kmajor ? (32u >> 4) : ((32u * C::kBCols) >> 4);  // desc units per K=32
-      const uint32_t full0 = opaque_u32(smem_u32(&full[0])), empty0 = opaque_u32(smem_u32(&empty[0]));
-      const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
+      const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+      const uint32_t tfull0 = smem_u32(&tfull[0]), tempty0 = smem_u32(&tempty[0]);
       uint32_t stage = 0, phase = 0, acc = 0, accph = 0, kiter = 0;
-      const int my_kblocks = ((total_tiles - cluster_id + num_clusters - 1) / num_clusters) * kbc;
-      for (int i = 0; i < my_kblocks; ++i) {
-        mbar_wait_addr(tempty0 + 8 * acc, accph ^ 1);
-        trace_stamp(p.trace, kEvMmaTempty, kiter);
-        mbar_wait_addr(full0 + 8 * stage, phase);
-        trace_stamp(p.trace, kEvMmaFull, kiter);
-        tc_fence_after();
-        const uint64_t ad = a_desc0 + ((stage * kStageBytesA) >> 4);
-        const uint64_t bd = b_desc0 + ((stage * C::kStageBytesB) >> 4);
-        const uint32_t d_tmem = tmem_base + acc * C::kBN;
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+        const uint32_t idesc_t =
+            (C::kHalfTiles && decode_tile<kCG, kBN>(t, 0, tab_tile, tab_row, tab_size, tab_crow, G).half)
+                ? idesc_half
+                : idesc;
+        for (int kb = 0; kb < kbc; ++kb) {
+          mbar_wait_addr(tempty0 + 8 * acc, accph ^ 1);
+          if (lane == 0) trace_stamp(p.trace, kEvMmaTempty, kiter);
+          mbar_wait_addr(full0 + 8 * stage, phase);
+          if (lane == 0) trace_stamp(p.trace, kEvMmaFull, kiter);
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + ((stage * kStageBytesA) >> 4);
+          const uint64_t bd = b_desc0 + ((stage * C::kStageBytesB) >> 4);
+          const uint32_t d_tmem = tmem_base + acc * C::kBN;
+          if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < BK / 32; ++k)
-          mma_f8f6f4<kCG>(d_tmem, ad + static_cast<uint64_t>(k * (32 >> 4)), bd + static_cast<uint64_t>(k * b_kstep),
-                          idesc, k > 0 ? 1u : 0u);
-        mma_commit_addr<kCG>(empty0 + 8 * stage);  // smem slot free (both CTAs) once these MMAs retire
-        mma_commit_addr<kCG>(tfull0 + 8 * acc);    // k-block partial ready for promotion (both CTAs)
-        trace_stamp(p.trace, kEvMmaIssued, kiter++);
-        if (++stage == S) { stage = 0; phase ^= 1; }
-        if (++acc == C::kNumAcc) { acc = 0; accph ^= 1; }
+            for (int k = 0; k < BK / 32; ++k)
+              mma_f8f6f4<kCG>(d_tmem, ad + static_cast<uint64_t>(k * (32 >> 4)),
+                              bd + static_cast<uint64_t>(k * b_kstep), idesc_t, k > 0 ? 1u : 0u);
+            mma_commit_addr<kCG>(empty0 + 8 * stage);  // smem slot free (both CTAs) once these MMAs retire
+            mma_commit_addr<kCG>(tfull0 + 8 * acc);    // k-block partial ready for promotion (both CTAs)
+          }
+          __syncwarp();
+          if (lane == 0) trace_stamp(p.trace, kEvMmaIssued, kiter);
+          ++kiter;
+          if (++stage == S) { stage = 0; phase ^= 1; }
+          if (++acc == C::kNumAcc) { acc = 0; accph ^= 1; }
+        }
       }
     }
     __syncwarp();
@@ -399,6 +427,103 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int rp = sa_row_prev(T.row0, rb);
+      if (C::kHalfTiles && T.half) {
+        // ===== half tile: this CTA's 64 rows x 256 columns in 128 TMEM columns.
+        // TMEM lanes 64..127 hold the tile's upper 128 columns of rows 0..63, so
+        // quarter q owns row 32 (q & 1) + lane, tile columns 128 (q >> 1) + 64 half + [0, 64).
+        const int hrow = 32 * (q & 1) + lane;
+        const int hcol = 128 * (q >> 1) + 64 * half;
+        mbar_wait_addr(sfull0 + 8 * sab, saph);
+        const uint32_t hsa = sSA0 + sab * p.sa_buf_bytes + static_cast<uint32_t>(rp + hrow) * rb;
+        const uint32_t hsb = sSB0 + sab * kSbBufBytes + 4u * static_cast<uint32_t>((q >> 1) * kbc);
+        float hacc[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) hacc[i] = 0.0f;
+        float hs_next = __fmul_rn(ld_shared_f32(hsa), ld_shared_f32(hsb));
+        for (int kb = 0; kb < kbc; ++kb) {
+          const float s = hs_next;
+          if (kb + 1 < kbc) hs_next = __fmul_rn(ld_shared_f32(hsa + 4u * (kb + 1)), ld_shared_f32(hsb + 4u * (kb + 1)));
+          mbar_wait_addr(tfull0 + 8 * acc_i, accph);
+          tc_fence_after();
+          const uint32_t tempty_b = tempty0 + 8 * acc_i;
+          const uint32_t taddr = tmem_base + t_lane + acc_i * C::kBN + 64u * half;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(taddr + 32 * c, v);
+            tmem_wait_ld_dep(v);
+            if (c == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_leader_addr(tempty_b);
+            }
+            if constexpr (kExact) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                hacc[32 * c + i] = __fadd_rn(hacc[32 * c + i], __fmul_rn(__uint_as_float(v[i]), s));
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2)
+                ffma2(hacc[32 * c + i], hacc[32 * c + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]), s);
+            }
+          }
+          ++kiter;
+          if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_addr(sempty0 + 8 * sab);
+        if (++sab == 2) { sab = 0; saph ^= 1; }
+        // epilogue: one pass, 4 staging chunks of 64 rows x 64 columns (8 KB each); each
+        // CTA stores its own <= 64 rows with the pool (64-row block plan, descriptors.py:95-106)
+        const int lg = T.valid > 0 ? 31 - __clz(T.valid) : 0;
+        const int d = 1 << lg;
+        constexpr uint32_t kHalfChunk = kChunkBytesC / 2;
+        if (ptid == 0) bulk_wait_read0();
+        named_bar_sync(1, 32 * kNumPromoWarps);
+        {
+          const uint32_t base = smem_u32(sC) + static_cast<uint32_t>(hcol >> 6) * kHalfChunk + hrow * 128u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t w0 = pack_bf16x2(hacc[8 * j + 0], hacc[8 * j + 1]);
+            const uint32_t w1 = pack_bf16x2(hacc[8 * j + 2], hacc[8 * j + 3]);
+            const uint32_t w2 = pack_bf16x2(hacc[8 * j + 4], hacc[8 * j + 5]);
+            const uint32_t w3 = pack_bf16x2(hacc[8 * j + 6], hacc[8 * j + 7]);
+            const uint32_t c16 = kSwizzleC ? static_cast<uint32_t>(j ^ (hrow & 7)) : static_cast<uint32_t>(j);
+            st_shared_v4(base + c16 * 16u, w0, w1, w2, w3);
+          }
+          fence_proxy_async_smem();
+        }
+        named_bar_sync(1, 32 * kNumPromoWarps);
+        if (ptid == 0 && T.valid > 0) {
+          for (int ch = 0; ch < 4; ++ch) {
+            const int col = T.n0 + 64 * ch;
+            if (col >= p.N) break;
+            const uint8_t* chunk = sC + ch * kHalfChunk;
+            tma_store_2d(&p.tmap_c[lg], chunk, col, T.crow0);
+            if (T.valid != BM / 2)
+              tma_store_2d(&p.tmap_c[lg], chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
+                           T.crow0 + T.valid - d);
+          }
+          bulk_commit();
+          if (p.tile_map) {
+            for (int sub = 0; sub < 2; ++sub) {
+              const int n0 = T.n0 + 128 * sub;
+              if (n0 >= p.N) continue;
+              int32_t* rec = p.tile_map + ((static_cast<int64_t>(t) * kCG + rank) * 2 + sub) * TAGG_TILE_MAP_FIELDS;
+              rec[0] = T.g;
+              rec[1] = T.mt;
+              rec[2] = n0;
+              rec[3] = T.row0;
+              rec[4] = T.valid;
+              rec[5] = d;
+              rec[6] = T.crow0;
+              rec[7] = T.valid - d;
+              rec[8] = T.crow0 + T.valid - d;
+            }
+          }
+        }
+        continue;
+      }
       mbar_wait_addr(sfull0 + 8 * sab, saph);
       // this thread's S_A row in the over-fetched window and its S_B column, both in smem
       const uint32_t sa_row = sSA0 + sab * p.sa_buf_bytes + static_cast<uint32_t>(rp + r) * rb;

@@ -52,8 +52,13 @@ def test_tile_map_is_bit_exact(name, tile):
     cfg, ops, _ = _cfg_ops(case)
     run = tg.run_adaptive(cfg, ops, tile=tile)
     got = sorted(tuple(int(x) for x in r) for r in run.tile_map)
-    want = sorted(oplan.tile_map(cfg.group_sizes, cfg.n))
+    want = sorted(oplan.kernel_tile_map(cfg.group_sizes, cfg.n, tile))
     assert got == want
+    # the rows each group's pieces write are exactly the reference tile loop's rows
+    covered = sorted({(r[0], r[2], row) for r in got for row in range(r[6], r[6] + r[4])})
+    ref = sorted({(r[0], r[2], row) for r in oplan.tile_map(cfg.group_sizes, cfg.n)
+                  for row in range(r[6], r[6] + r[4])})
+    assert covered == ref
 
 
 @pytest.mark.parametrize("name", ["c1", "k640", "perexpert"])
@@ -114,7 +119,7 @@ def test_residual_sweep_every_residue_small(tile):
         run = tg.run_adaptive(cfg, tg.GroupedOperands(ac, asc, bc, bsc), tile=tile)
         assert_parity(run.c_bits, oracle_c(ac, asc, bc, bsc, sizes), label=f"r0={r0}")
         got = sorted(tuple(int(x) for x in rr) for rr in run.tile_map)
-        assert got == sorted(oplan.tile_map(sizes, n))
+        assert got == sorted(oplan.kernel_tile_map(sizes, n, tile))
 
 
 def _synthetic(sizes, n, k, seed, layout="kn"):

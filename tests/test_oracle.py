@@ -158,3 +158,19 @@ def test_tile_map_restatement_covers_rows_exactly():
         off = sum(sizes[:g])
         assert bg + d <= off + sizes[g]
     assert np.all(hits >= 1)
+
+
+@pytest.mark.parametrize("sizes", [(1, 67, 128, 255, 0, 256, 129), (64, 65, 192, 320, 384, 3), (128 * 3 + 77,)])
+def test_kernel_tile_map_stores_exactly_the_reference_rows(sizes):
+    """The kernel's half-tile pieces (64-row reference plans) cover exactly the rows of
+    the reference tile loop and never a row past M_g."""
+    n = 256
+    ker = oplan.kernel_tile_map(sizes, n)
+    ref = oplan.tile_map(sizes, n)
+    rows = lambda recs: sorted({(r[0], r[2], x) for r in recs for x in range(r[6], r[6] + r[4])})  # noqa: E731
+    assert rows(ker) == rows(ref)
+    for g, t, n0, r0, valid, d, ag, bs, bg in ker:
+        off = sum(sizes[:g])
+        assert 1 <= valid and d <= valid < 2 * d
+        assert ag + d <= off + sizes[g] and bg + d <= off + sizes[g]
+        assert bg - ag == valid - d == bs

@@ -212,12 +212,23 @@ void run(const char* name, const P& p, unsigned long long* d_out, float* sink) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  for (int it = 0; it < 2; ++it) cudaLaunchKernelEx(&cfg, gemm<MODE, LOAD, X>, p, reps, d_out, sink);
+  cudaLaunchKernelEx(&cfg, gemm<MODE, LOAD, X>, p, reps, d_out, sink);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int it = 0; it < 5; ++it) cudaLaunchKernelEx(&cfg, gemm<MODE, LOAD, X>, p, reps, d_out, sink);
+  cudaEventRecord(e1);
   const cudaError_t e = cudaDeviceSynchronize();
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= 5;
+  const double tflops = 74.0 * reps * KB * 2.0 * 256 * 256 * 128 / (ms * 1e-3) / 1e12;
   std::vector<unsigned long long> h(148);
   cudaMemcpy(h.data(), d_out, 148 * 8, cudaMemcpyDeviceToHost);
   const double mx = *std::max_element(h.begin(), h.end());
-  printf("%-40s k-block period %7.1f clk  %s\n", name, mx / (reps * KB), e == cudaSuccess ? "" : cudaGetErrorString(e));
+  printf("%-40s k-block period %7.1f clk  %7.1f TFLOP/s  (%.0f MHz) %s\n", name, mx / (reps * KB), tflops,
+         mx / (ms * 1e3), e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
 int main() {

@@ -43,18 +43,27 @@ for name, sizes, n, k, G, bl in shapes:
                                          flags, torch.cuda.current_stream().cuda_stream)
         assert rc == 0, rc
 
+    # ABBA-interleaved rounds: power/boost state drifts over a run, so libraries are
+    # timed alternately and each reports its median over rounds.
+    loaded = [load(path) for path in libs]
+    times = {path: [] for path in libs}
+    order = list(range(len(libs)))
+    for rnd in range(6):
+        seq = order if rnd % 2 == 0 else order[::-1]
+        for i in seq:
+            L = loaded[i]
+            for _ in range(2):
+                run()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(10):
+                run()
+            e.record()
+            torch.cuda.synchronize()
+            times[libs[i]].append(s.elapsed_time(e) / 10)
     for path in libs:
-        L = load(path)
-        for _ in range(3):
-            run()
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for _ in range(20):
-            run()
-        e.record()
-        torch.cuda.synchronize()
-        ms = s.elapsed_time(e) / 20
+        ms = sorted(times[path])[len(times[path]) // 2]
         tag = path.rsplit("/", 1)[-1]
         print(f"{name:14s} {tag:22s} {ms * 1e3:9.1f} us  {P.flops[0] / ms / 1e9:8.1f} TFLOP/s", flush=True)
     del P
