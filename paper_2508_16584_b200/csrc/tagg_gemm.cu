@@ -277,8 +277,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     // the A / B k-blocks (lane 0).
     uint32_t stage = 0, phase = 0, sab = 0, saph = 0, kiter = 0;
     const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
-    const uint32_t full0 = opaque_u32(smem_u32(&full[0])), empty0 = opaque_u32(smem_u32(&empty[0]));
-    const uint32_t sA0 = opaque_u32(smem_u32(sA)), sB0 = opaque_u32(smem_u32(sB));
+    const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
     for (int t = cluster_id; t < total_tiles; t += num_clusters) {
       const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
@@ -317,26 +317,30 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       }
       if (++sab == 2) { sab = 0; saph ^= 1; }
       // ---- A / B k-blocks.  This CTA stages its 128 rows of A and its B column share;
-      // completion is counted on the leader's barrier.
-      if (lane == 0) {
+      // completion is counted on the leader's barrier.  The whole warp runs the loop
+      // (warp-uniform operands, no per-lane waterfall); one elected lane issues.
+      {
         const int nb = T.n0 + rank * C::kBCols;
         for (int kb = 0; kb < kbc; ++kb) {
           mbar_wait_addr(empty0 + 8 * stage, phase ^ 1);
-          trace_stamp(p.trace, kEvProdEmpty, kiter++);
+          if (lane == 0) trace_stamp(p.trace, kEvProdEmpty, kiter);
+          ++kiter;
           const uint32_t fb = full0 + 8 * stage;
-          if (dbg & kDbgNoLoad) {
-            if (is_leader) mbar_arrive_addr(fb);
-          } else {
-            if (is_leader) mbar_arrive_expect_tx_addr(fb, C::kStageTx);
-            const int cb0 = p.b_kmajor ? kb * BK : nb;
-            const int cb1 = p.b_kmajor ? nb : kb * BK;
-            tma_load_2d_u32<kCG>(&p.tmap_a, fb, sA0 + stage * kStageBytesA, kb * BK, T.row0);
-            tma_load_3d_u32<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb);
+          if (elect_one()) {
+            if (dbg & kDbgNoLoad) {
+              if (is_leader) mbar_arrive_addr(fb);
+            } else {
+              if (is_leader) mbar_arrive_expect_tx_addr(fb, C::kStageTx);
+              const int cb0 = p.b_kmajor ? kb * BK : nb;
+              const int cb1 = p.b_kmajor ? nb : kb * BK;
+              tma_load_2d_u32<kCG>(&p.tmap_a, fb, sA0 + stage * kStageBytesA, kb * BK, T.row0);
+              tma_load_3d_u32<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb);
+            }
           }
+          __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
-      __syncwarp();
     }
     // Producer tail: wait until every issued stage has been consumed, so no MMA
     // commit can still target this CTA's barriers after it exits.
