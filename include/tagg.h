@@ -126,8 +126,8 @@ int64_t tagg_pad_rows(const int64_t* group_sizes, int G, int64_t block_rows);
 
 const char* tagg_error_string(int code);
 /* Diagnostics only: subsequent tagg_grouped_gemm_fp8 launches stamp clock64()
-   at 8 pipeline events for the first 1024 k-block iterations of CTAs 0 and 1
-   into buf (DEVICE u64 [2][8][1024]); NULL (the default) disables it. */
+   at 10 pipeline events for the first 1024 k-block iterations of CTAs 0 and 1
+   into buf (DEVICE u64 [2][10][1024]); NULL (the default) disables it. */
 void tagg_debug_trace(void* buf);
 int tagg_version(void);
 

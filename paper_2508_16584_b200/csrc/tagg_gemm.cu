@@ -106,9 +106,9 @@ struct Cfg {
 // Diagnostics trace: stamps of the first kTraceLen k-block iterations of CTAs 0 and 1.
 // Compiled in only with -DTAGG_TRACE (libtagg_trace.so, `make trace`; tools/trace.py).
 constexpr int kTraceLen = 1024;
-constexpr int kTraceEvents = 8;
+constexpr int kTraceEvents = 10;
 enum TraceEv { kEvMmaTempty = 0, kEvMmaFull, kEvMmaIssued, kEvProdEmpty, kEvPromoFull, kEvPromoFreed, kEvPromoDone,
-               kEvPromo2Full };
+               kEvPromo2Full, kEvEpiStart, kEvEpiEnd };
 __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int ev, uint32_t i) {
 #ifdef TAGG_TRACE
   if (tr != nullptr && blockIdx.x < 2 && i < static_cast<uint32_t>(kTraceLen))
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
     const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
-    uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0;
+    uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0, tiles_done = 0;
 #ifdef TAGG_TRACE
     const bool tr_a = p.trace != nullptr && pw == 0 && lane == 0;
     const bool tr_b = p.trace != nullptr && pw == 4 && lane == 0;
@@ -594,6 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       if (lane == 0) mbar_arrive_addr(sempty0 + 8 * sab);
       if (++sab == 2) { sab = 0; saph ^= 1; }
 
+      if (tr_a) trace_stamp(p.trace, kEvEpiStart, tiles_done);
       // ---- epilogue: bf16 -> swizzled smem staging (2 chunks of 64 columns)
       //      -> TMA stores from the 8-height pool, dual phase for residual rows.
       //      kBN=128: one pass, warp half h writes chunk h (its 64 columns).
@@ -656,6 +657,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           }
         }
       }
+      if (tr_a) trace_stamp(p.trace, kEvEpiEnd, tiles_done);
+      ++tiles_done;
     }
     if (ptid == 0) bulk_wait0();
   }
@@ -842,7 +845,7 @@ unsigned long long* g_trace = nullptr;
 }
 
 // Diagnostics: the next launches stamp clock64 per k-block event of CTAs 0 and 1
-// into buf ([2][8][1024] u64, device); NULL turns tracing off.
+// into buf ([2][10][1024] u64, device); NULL turns tracing off.
 extern "C" void tagg_debug_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
 
 // Capacity (records) a tile_map buffer needs: an upper bound valid for every

@@ -16,9 +16,10 @@ for name, (res, args) in _lib.SIGNATURES.items():
     fn = getattr(L, name)
     fn.restype, fn.argtypes = res, args
 
-EV = ["mma_tempty", "mma_full", "mma_issued", "prod_empty", "promo_full", "promo_freed", "promo_done", "promo2_full"]
+EV = ["mma_tempty", "mma_full", "mma_issued", "prod_empty", "promo_full", "promo_freed", "promo_done", "promo2_full",
+      "epi_start", "epi_end"]
 dev = torch.device("cuda", 0)
-buf = torch.zeros((2, 8, 1024), dtype=torch.int64, device=dev)
+buf = torch.zeros((2, 10, 1024), dtype=torch.int64, device=dev)
 
 
 def run(P, flags, G):
@@ -46,12 +47,19 @@ def report(tr, lo, hi, label):
     print(f"--- {label}: k-block iterations [{lo},{hi}) of CTA 0, clk (median / p10 / p90)")
     for k, v in rows.items():
         print(f"  {k:38s} {np.median(v):8.0f} {np.percentile(v, 10):8.0f} {np.percentile(v, 90):8.0f}")
+    es, ee = t[EV.index("epi_start")], t[EV.index("epi_end")]
+    nt = int((ee > 0).sum())
+    if nt > 1:
+        dur = ee[:nt] - es[:nt]
+        print(f"  epilogue per tile (clk): median {np.median(dur):.0f} over {nt} tiles")
     t1 = tr[1].astype(np.float64)
     v = t1[EV.index("promo_full"), lo:hi] - t1[EV.index("promo_full"), lo - 1:hi - 1]
     print(f"  {'CTA1 promo full period':38s} {np.median(v):8.0f}")
 
 
 cases = [("sq8192", [(8192,)], 8192, 8192, 1), ("sweep_r64", [tuple(128 * g + 64 for g in range(8))], 4096, 7168, 8)]
+if len(sys.argv) > 1 and sys.argv[1] == "qdown":
+    cases = [("qdown", [tuple([2048] * 128)], 4096, 1536, 128)]
 if len(sys.argv) > 1 and sys.argv[1] == "longk":
     # one pair tile per cluster, 256 k-blocks per tile: no tile transitions in the window
     cases = [("longk", [(256 * 74,)], 256, 8192, 1)]
@@ -66,5 +74,5 @@ for name, sizes, n, k, G in cases:
         run(P, flags, G)
         torch.cuda.synchronize()
         L.tagg_debug_trace(None)
-        report(buf.cpu().numpy(), 8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60}[name], f"{name} {label}")
+        report(buf.cpu().numpy(), 8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60, "qdown": 600}[name], f"{name} {label}")
     del P
