@@ -86,6 +86,7 @@ struct Params {
   int64_t sb_sg, sb_skb, sb_snb;
   int32_t G, N, K, kb_count, n_tiles, sa_rb, b_kmajor, b_shared;
   uint32_t stages, sa_buf_bytes;
+  uint32_t epi_passes;  // 256-column tiles: 1 = 64 KB staging, all 4 chunks at once; 2 = 32 KB, two passes
   uint32_t off_a, off_b, off_c, off_sa, off_sb, off_tab, off_bar;
   uint32_t dbg;
 };
@@ -601,15 +602,16 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       //      kBN=256: pass h, warp half h writes both chunks (its 128 columns).
       const int lg = T.valid > 0 ? 31 - __clz(T.valid) : 0;  // pool index: d = 2^floor(log2 valid)
       const int d = 1 << lg;
-      constexpr int kPasses = kBN / 128;
-#pragma unroll
-      for (int pass = 0; pass < kPasses; ++pass) {
+      // kBN=256 with epi_passes == 1: one pass, all 8 warps write, chunk 2 half + j / 8
+      const int passes = (kBN == 256) ? static_cast<int>(p.epi_passes) : 1;
+      for (int pass = 0; pass < passes; ++pass) {
         if (ptid == 0) bulk_wait_read0();  // earlier stores have finished reading the staging
         named_bar_sync(1, 32 * kNumPromoWarps);
-        if (kCPT == 64 || half == pass) {
+        if (kCPT == 64 || passes == 1 || half == pass) {
+          const int chunk0 = (kCPT == 64) ? half : (passes == 1 ? 2 * half : 0);
 #pragma unroll
           for (int j = 0; j < kCPT / 8; ++j) {
-            const int chunk = (kCPT == 64) ? half : (j >> 3);
+            const int chunk = chunk0 + ((kCPT == 64) ? 0 : (j >> 3));
             const int pc = j & 7;
             const uint32_t w0 = pack_bf16x2(acc[8 * j + 0], acc[8 * j + 1]);
             const uint32_t w1 = pack_bf16x2(acc[8 * j + 2], acc[8 * j + 3]);
@@ -623,7 +625,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         }
         named_bar_sync(1, 32 * kNumPromoWarps);
         if (ptid == 0 && T.valid > 0) {
-          for (int ch = 0; ch < 2; ++ch) {
+          const int nchunks = (kBN == 256 && passes == 1) ? 4 : 2;
+          for (int ch = 0; ch < nchunks; ++ch) {
             const int col = T.n0 + 128 * pass + 64 * ch;
             if (col >= p.N) break;
             const uint8_t* chunk = sC + ch * kChunkBytesC;
@@ -639,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           bulk_commit();
           if (p.tile_map) {
             for (int sub = 0; sub < C::kBN / 128; ++sub) {
-              if (sub != pass) continue;
+              if (passes > 1 && sub != pass) continue;
               const int n0 = T.n0 + 128 * sub;
               if (n0 >= p.N) continue;
               int32_t* rec = p.tile_map + ((static_cast<int64_t>(t) * kCG + rank) * (C::kBN / 128) + sub) *
@@ -784,7 +787,8 @@ int gcd_int(int a, int b) {
 }  // namespace
 
 // Smem layout for a given stage count; returns total bytes (incl. alignment slack).
-static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_acc, uint32_t stage_bytes_b) {
+static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_acc, uint32_t stage_bytes_b,
+                            uint32_t staging_bytes) {
   // row_prev < 16 / gcd(rb, 16): the residue class of row0*rb mod 16 has that period
   const int rp_max = 16 / gcd_int(rb, 16) - 1;
   const uint32_t sa_buf = align_up(static_cast<uint32_t>(((rp_max + BM) * rb + 15) & ~15), 128);
@@ -793,7 +797,7 @@ static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_a
   p.off_a = 0;
   p.off_b = stages * kStageBytesA;
   p.off_c = p.off_b + stages * stage_bytes_b;
-  p.off_sa = p.off_c + kCStagingBytes;
+  p.off_sa = p.off_c + staging_bytes;
   p.off_sb = p.off_sa + 2 * sa_buf;
   p.off_tab = p.off_sb + 2 * kSbBufBytes;
   const uint32_t tab_bytes = align_up(4u * static_cast<uint32_t>(2 * (G + 1) + 2 * G), 16);
@@ -920,8 +924,22 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   // bits 12-15 of flags cap the stage count (diagnostics); 0 = as many as fit
   const uint32_t stage_cap = (flags >> 12) & 0xFu;
   uint32_t stages = stage_cap ? std::min<uint32_t>(stage_cap, kMaxStages) : kMaxStages;
+  // 256-column tiles: a 64 KB C staging (single-pass epilogue, whose TMA stores then
+  // overlap the next tile's k-loop) when that still leaves >= 3 pipeline stages
+  // (measured: 3 stages feed the MMA as well as 4); else 32 KB and two passes.
+  p.epi_passes = 2;
+  if (bn == 256) {
+    uint32_t s1 = stages;
+    for (; s1 >= 3; --s1)
+      if (smem_layout(p, s1, G, rb, num_acc, stage_bytes_b, 2 * kCStagingBytes) <= 232448) break;
+    if (s1 >= 3) {
+      stages = s1;
+      p.epi_passes = 1;
+    }
+  }
+  const uint32_t staging = p.epi_passes == 1 ? 2 * kCStagingBytes : kCStagingBytes;
   for (; stages >= 2; --stages) {
-    smem_bytes = smem_layout(p, stages, G, rb, num_acc, stage_bytes_b);
+    smem_bytes = smem_layout(p, stages, G, rb, num_acc, stage_bytes_b, staging);
     if (smem_bytes <= 232448) break;
   }
   if (stages < 2) return TAGG_ERR_UNSUPPORTED;
