@@ -559,14 +559,14 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           continue;
         }
         const uint32_t taddr = tmem_base + t_lane + acc_i * C::kBN + half * kCPT;
-        // TMEM drain, 32 columns at a time; the buffer is handed back as soon as the
+        // TMEM drain, 64 columns at a time; the buffer is handed back as soon as the
         // last chunk has landed in registers.
-        constexpr int kChunks = kCPT / 32;
+        constexpr int kChunks = kCPT / 64;
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(taddr + 32 * c, v);
-          tmem_wait_ld_dep(v);
+          uint32_t v[64];
+          tmem_ld_32x32b_x64(taddr + 64 * c, v);
+          tmem_wait_ld_dep64(v);
           if (c + 1 == kChunks) {
             tc_fence_before();
             __syncwarp();
@@ -576,15 +576,15 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             if (tr_a) trace_stamp(p.trace, kEvPromoFreed, kiter);
           }
           if (dbg & kDbgNoMath) {
-            acc[32 * c] += __uint_as_float(v[c]);
+            acc[64 * c] += __uint_as_float(v[c]);
           } else if constexpr (kExact) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              acc[32 * c + i] = __fadd_rn(acc[32 * c + i], __fmul_rn(__uint_as_float(v[i]), s));
+            for (int i = 0; i < 64; ++i)
+              acc[64 * c + i] = __fadd_rn(acc[64 * c + i], __fmul_rn(__uint_as_float(v[i]), s));
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; i += 2)
-              ffma2(acc[32 * c + i], acc[32 * c + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]), s);
+            for (int i = 0; i < 64; i += 2)
+              ffma2(acc[64 * c + i], acc[64 * c + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]), s);
           }
         }
         if (tr_a) trace_stamp(p.trace, kEvPromoDone, kiter);
