@@ -95,6 +95,12 @@ int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa, int64_t m
 /* Upper bound on the tile count, to size tile_map (no device data needed). */
 int64_t tagg_max_tiles(int64_t m_alloc, int G, int N);
 
+/* CTA clusters (pairs, or single CTAs with TAGG_FLAG_SINGLE_CTA) a launch with these
+   sizes uses on the current device.  The 256x256 pair tile balances its last wave
+   with it: when T mod clusters <= clusters / 2 for T scheduled tiles, those last tiles
+   each run as two 128-row half tiles (oracle/plan.py: kernel_tile_map). */
+int tagg_launch_clusters(int64_t m_alloc, int G, int N, uint32_t flags);
+
 /*
  * Baseline K2 (engine.py:369-373): copy each group into a 128-row-aligned
  * slot, A pad rows = 0, S_A pad rows = 1.0.  a_pad / sa_pad need

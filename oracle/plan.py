@@ -67,7 +67,7 @@ def format_plan(plans) -> str:
     return "\n".join(lines)
 
 
-def kernel_tile_map(group_sizes, n: int, tile: str = "pair_n256", c_row_offsets=None):
+def kernel_tile_map(group_sizes, n: int, tile: str = "pair_n256", c_row_offsets=None, num_pairs=None):
     """The store geometry the B200 kernel uses, stated with the reference planner.
 
     Every stored piece follows plan_two_phase (descriptors.py:72-106) for its block
@@ -76,37 +76,66 @@ def kernel_tile_map(group_sizes, n: int, tile: str = "pair_n256", c_row_offsets=
     last pair tile with at most 128 valid rows as a HALF tile (one tcgen05.mma M=128
     per K step, 64 rows per CTA), and each CTA stores its 64-row piece with the
     reference plan at block_rows = 64: a full piece is one 64-row store, a residual
-    piece the two-phase store.  The mapping of rows to groups (which C rows each
-    piece writes, never a row past M_g) is the reference's in every case.
+    piece the two-phase store.  Tail balancing (num_pairs = the launch's CTA pairs,
+    tagg_launch_clusters): when T mod num_pairs <= num_pairs / 2 for T scheduled
+    tiles, the last T mod num_pairs tiles in schedule order each run as two half
+    tiles of 128 rows (64-row pieces again).  The mapping of rows to groups (which C
+    rows each piece writes, never a row past M_g) is the reference's in every case.
     Records: (g, m_tile, n0, a_row0, valid, d, phaseA_gmem_row, phaseB_smem_row,
     phaseB_gmem_row), m_tile = the reference's 128-row tile index.
     """
     if tile != "pair_n256":
         return tile_map(group_sizes, n, c_row_offsets=c_row_offsets)
+    sizes = [int(x) for x in group_sizes]
+    offs, coffs, o = [], [], 0
+    for g, rows in enumerate(sizes):
+        offs.append(o)
+        coffs.append(o if c_row_offsets is None else int(c_row_offsets[g]))
+        o += rows
+    ntn = -(-n // 256)
+    # the kernel's static schedule (decode_tile): groups in order, inside a group
+    # super-rows of 8 pair m-tiles with n-tiles outer
+    sched = []
+    for g, rows in enumerate(sizes):
+        pt = -(-rows // 256)
+        for local in range(pt * ntn):
+            sr = local // (8 * ntn)
+            h = min(8, pt - sr * 8)
+            loc = local - sr * 8 * ntn
+            sched.append((g, sr * 8 + loc % h, (loc // h) * 256))
+    T = len(sched)
+    x = 0
+    if num_pairs:
+        tail = T % num_pairs
+        x = tail if (tail and 2 * tail <= num_pairs) else 0
+
+    def piece(g, mt, n0, r0, v):
+        d = 1 << (v.bit_length() - 1)
+        for c in (n0, n0 + 128):
+            if c < n:
+                recs.append((g, mt, c, offs[g] + r0, v, d, coffs[g] + r0, v - d, coffs[g] + r0 + v - d))
+
     recs = []
-    off = 0
-    for g, rows in enumerate(group_sizes):
-        rows = int(rows)
-        coff = off if c_row_offsets is None else int(c_row_offsets[g])
-        for pm in range(-(-rows // 256)):
-            base = 256 * pm
-            if rows - base <= 128:  # half tile: two 64-row pieces
+    for idx, (g, pm, n0) in enumerate(sched):
+        rows, base = sizes[g], 256 * pm
+        if idx >= T - x:  # tail balancing: two half tiles of 128 rows
+            for sub in range(2):
                 for j in range(2):
-                    r0 = base + 64 * j
+                    r0 = base + 128 * sub + 64 * j
                     v = min(64, rows - r0)
-                    if v <= 0:
-                        continue
-                    d = 1 << (v.bit_length() - 1)
-                    for n0 in range(0, n, 128):
-                        recs.append((g, 2 * pm, n0, off + r0, v, d, coff + r0, v - d, coff + r0 + v - d))
-            else:
-                for t in (2 * pm, 2 * pm + 1):
-                    r0 = 128 * t
-                    v = min(128, rows - r0)
-                    d = 1 << (v.bit_length() - 1)
-                    for n0 in range(0, n, 128):
-                        recs.append((g, t, n0, off + r0, v, d, coff + r0, v - d, coff + r0 + v - d))
-        off += rows
+                    if v > 0:
+                        piece(g, 2 * pm + sub, n0, r0, v)
+        elif rows - base <= 128:  # half tile: two 64-row pieces
+            for j in range(2):
+                r0 = base + 64 * j
+                v = min(64, rows - r0)
+                if v > 0:
+                    piece(g, 2 * pm, n0, r0, v)
+        else:
+            for t in (2 * pm, 2 * pm + 1):
+                r0 = 128 * t
+                v = min(128, rows - r0)
+                piece(g, t, n0, r0, v)
     return recs
 
 

@@ -25,6 +25,7 @@ SIGNATURES = {
                                       c_i64, c_vp, c_int, c_int, c_int, c_vp, c_i64, c_i64, c_vp, c_vp,
                                       c_u32, c_vp]),
     "tagg_max_tiles": (c_i64, [c_i64, c_int, c_int]),
+    "tagg_launch_clusters": (c_int, [c_i64, c_int, c_int, c_u32]),
     "tagg_pad_groups": (c_int, [c_vp, c_i64, c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "tagg_unpad_rows": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_i64, c_vp]),
     "tagg_padded_rows_bound": (c_i64, [c_i64, c_int]),

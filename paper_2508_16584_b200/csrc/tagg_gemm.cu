@@ -167,6 +167,35 @@ __device__ __forceinline__ Tile decode_tile(int t, int rank, const int32_t* tab_
   return T;
 }
 
+// Tail balancing.  The persistent grid walks "units": the T scheduled tiles, except
+// that when the last wave would be at most half full (T mod P <= P/2 for P pairs),
+// its x = T mod P tiles are each split into two HALF tiles of 128 rows (sub 0: rows
+// [pm*256, +128), sub 1: [pm*256 + 128, +128)), so the last wave is 2x half-cost
+// units instead of x full tiles on an otherwise idle GPU (the residual sweep: 320
+// tiles on 74 pairs -> 4.5 instead of 5 tile times).
+__host__ __device__ __forceinline__ int tail_split_count(int T, int P, bool enabled) {
+  const int tail = T % P;
+  return (enabled && tail != 0 && 2 * tail <= P) ? tail : 0;
+}
+
+template <int kCG, int kBN>
+__device__ __forceinline__ Tile decode_unit(int u, int T, int x, int rank, const int32_t* tab_tile,
+                                            const int32_t* tab_row, const int32_t* tab_size, const int32_t* tab_crow,
+                                            int G) {
+  if (!Cfg<kCG, kBN>::kHalfTiles || u < T - x) return decode_tile<kCG, kBN>(u, rank, tab_tile, tab_row, tab_size, tab_crow, G);
+  const int v = u - (T - x);
+  Tile U = decode_tile<kCG, kBN>((T - x) + (v >> 1), 0, tab_tile, tab_row, tab_size, tab_crow, G);
+  const int pm = U.mt >> 1;  // rank 0's slice: mt = 2 pm for full and half tiles alike
+  const int sub = v & 1;
+  const int r0 = pm * Cfg<kCG, kBN>::kTileM + BM * sub + (BM / 2) * rank;
+  U.half = true;
+  U.mt = 2 * pm + sub;
+  U.row0 = tab_row[U.g] + r0;
+  U.valid = min(BM / 2, tab_size[U.g] - r0);
+  U.crow0 = tab_crow[U.g] + r0;
+  return U;
+}
+
 // prefetch.py:50-72: smallest row_prev in [0, 16) that puts the window start
 // on a 16-byte boundary (the S_A base itself is 16-byte aligned).
 __device__ __forceinline__ int sa_row_prev(int64_t row0, int rb) {
@@ -281,8 +310,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
     const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
-    for (int t = cluster_id; t < total_tiles; t += num_clusters) {
-      const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
+    const int xs = tail_split_count(total_tiles, num_clusters, C::kHalfTiles);
+    for (int t = cluster_id; t < total_tiles + xs; t += num_clusters) {
+      const Tile T = decode_unit<kCG, kBN>(t, total_tiles, xs, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int gb = p.b_shared ? 0 : T.g;
       mbar_wait_addr(sempty0 + 8 * sab, saph ^ 1);
       // ---- S_B columns of the tile (engine.py:166-169: column block n // 128)
@@ -373,9 +403,10 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
       const uint32_t tfull0 = smem_u32(&tfull[0]), tempty0 = smem_u32(&tempty[0]);
       uint32_t stage = 0, phase = 0, acc = 0, accph = 0, kiter = 0;
-      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+      const int xs = tail_split_count(total_tiles, num_clusters, C::kHalfTiles);
+      for (int t = cluster_id; t < total_tiles + xs; t += num_clusters) {
         const uint32_t idesc_t =
-            (C::kHalfTiles && decode_tile<kCG, kBN>(t, 0, tab_tile, tab_row, tab_size, tab_crow, G).half)
+            (C::kHalfTiles && decode_unit<kCG, kBN>(t, total_tiles, xs, 0, tab_tile, tab_row, tab_size, tab_crow, G).half)
                 ? idesc_half
                 : idesc;
         for (int kb = 0; kb < kbc; ++kb) {
@@ -429,8 +460,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
 #else
     constexpr bool tr_a = false, tr_b = false;
 #endif
-    for (int t = cluster_id; t < total_tiles; t += num_clusters) {
-      const Tile T = decode_tile<kCG, kBN>(t, rank, tab_tile, tab_row, tab_size, tab_crow, G);
+    const int xs = tail_split_count(total_tiles, num_clusters, C::kHalfTiles);
+    for (int t = cluster_id; t < total_tiles + xs; t += num_clusters) {
+      const Tile T = decode_unit<kCG, kBN>(t, total_tiles, xs, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int rp = sa_row_prev(T.row0, rb);
       if (C::kHalfTiles && T.half) {
         // ===== half tile: this CTA's 64 rows x 256 columns in 128 TMEM columns.
@@ -854,9 +886,28 @@ extern "C" void tagg_debug_trace(void* buf) { g_trace = static_cast<unsigned lon
 
 // Capacity (records) a tile_map buffer needs: an upper bound valid for every
 // tile shape (one record per 128-row x 128-column store tile, incl. empty pair halves).
+// Persistent grid: one CTA (cg=1) or CTA pair (cg=2) per SM (pair), capped by the
+// tile bound (x2 for 256-column pair tiles: their tail balancing can split tiles in two).
+static int tagg_launch_clusters_impl(int sms, int64_t m_alloc, int G, int N, int cg, int bn) {
+  const int64_t n_tiles = (N + bn - 1) / bn;
+  int64_t bound = ((m_alloc + 128 * cg - 1) / (128 * cg) + G) * n_tiles;  // scheduled tiles
+  if (cg == 2 && bn == 256) bound *= 2;
+  return static_cast<int>(std::min<int64_t>(sms / cg, std::max<int64_t>(bound, 1)));
+}
+
+extern "C" int tagg_launch_clusters(int64_t m_alloc, int G, int N, uint32_t flags) {
+  if (m_alloc < 0 || G < 1 || N < 64) return TAGG_ERR_CONFIG;
+  const int sms = num_sms_for_current_device();
+  if (sms <= 0) return TAGG_ERR_CUDA;
+  const int cg = (flags & TAGG_FLAG_SINGLE_CTA) ? 1 : 2;
+  const int bn = (cg == 1 || (flags & TAGG_FLAG_TILE_N128)) ? 128 : 256;
+  return tagg_launch_clusters_impl(sms, m_alloc, G, N, cg, bn);
+}
+
 extern "C" int64_t tagg_max_tiles(int64_t m_alloc, int G, int N) {
   if (m_alloc < 0 || G < 1 || N < 1) return 0;
-  return ((m_alloc + 255) / 256 + G) * 2 * ((N + 255) / 256) * 2;
+  // x2: tail balancing may split up to every scheduled tile into two half-tile units
+  return ((m_alloc + 255) / 256 + G) * 2 * ((N + 255) / 256) * 2 * 2;
 }
 
 extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa, int64_t m_alloc,
@@ -979,9 +1030,7 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
       return TAGG_ERR_CUDA;
   }
 
-  // persistent grid: one CTA (cg=1) or CTA pair (cg=2) per SM (pair), capped by the tile bound
-  const int64_t tile_bound = ((m_alloc + 128 * cg - 1) / (128 * cg) + G) * p.n_tiles;  // scheduled tiles
-  const int grid = static_cast<int>(std::min<int64_t>(sms / cg, tile_bound)) * cg;
+  const int grid = tagg_launch_clusters_impl(sms, m_alloc, G, N, cg, bn) * cg;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool exact = (flags & TAGG_FLAG_EXACT_PROMOTION) != 0;
   cudaError_t e;

@@ -44,6 +44,12 @@ def test_golden_fixtures(name, mode):
     print(f"{name}/{mode}: {rep}")
 
 
+def _pairs(sizes, n):
+    """CTA pairs of a default-tile launch over these groups (tagg_launch_clusters)."""
+    from paper_2508_16584_b200._lib import lib
+    return lib().tagg_launch_clusters(int(sum(sizes)), len(sizes), n, 0)
+
+
 @pytest.mark.parametrize("name", CASES)
 @pytest.mark.parametrize("tile", ["1cta", "pair_n128", "pair_n256"])
 def test_tile_map_is_bit_exact(name, tile):
@@ -52,7 +58,7 @@ def test_tile_map_is_bit_exact(name, tile):
     cfg, ops, _ = _cfg_ops(case)
     run = tg.run_adaptive(cfg, ops, tile=tile)
     got = sorted(tuple(int(x) for x in r) for r in run.tile_map)
-    want = sorted(oplan.kernel_tile_map(cfg.group_sizes, cfg.n, tile))
+    want = sorted(oplan.kernel_tile_map(cfg.group_sizes, cfg.n, tile, num_pairs=_pairs(cfg.group_sizes, cfg.n)))
     assert got == want
     # the rows each group's pieces write are exactly the reference tile loop's rows
     covered = sorted({(r[0], r[2], row) for r in got for row in range(r[6], r[6] + r[4])})
@@ -119,7 +125,7 @@ def test_residual_sweep_every_residue_small(tile):
         run = tg.run_adaptive(cfg, tg.GroupedOperands(ac, asc, bc, bsc), tile=tile)
         assert_parity(run.c_bits, oracle_c(ac, asc, bc, bsc, sizes), label=f"r0={r0}")
         got = sorted(tuple(int(x) for x in rr) for rr in run.tile_map)
-        assert got == sorted(oplan.kernel_tile_map(sizes, n, tile))
+        assert got == sorted(oplan.kernel_tile_map(sizes, n, tile, num_pairs=_pairs(sizes, n)))
 
 
 def _synthetic(sizes, n, k, seed, layout="kn"):

@@ -20,7 +20,8 @@ flags = int(args[0], 0) if args else 0
 def load(path):
     L = ctypes.CDLL(path)
     for nm, (r, a) in _lib.SIGNATURES.items():
-        getattr(L, nm).restype, getattr(L, nm).argtypes = r, a
+        if hasattr(L, nm):
+            getattr(L, nm).restype, getattr(L, nm).argtypes = r, a
     return L
 dev = torch.device("cuda", 0)
 shapes = [
