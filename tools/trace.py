@@ -58,6 +58,9 @@ def report(tr, lo, hi, label):
 
 
 cases = [("sq8192", [(8192,)], 8192, 8192, 1), ("sweep_r64", [tuple(128 * g + 64 for g in range(8))], 4096, 7168, 8)]
+if len(sys.argv) > 1 and sys.argv[1] == "ds":
+    from bench import deepseek_gateup_sizes
+    cases = [("ds", [tuple(int(x) for x in deepseek_gateup_sizes(0)[1])], 4096, 7168, 32)]
 if len(sys.argv) > 1 and sys.argv[1] == "qdown":
     cases = [("qdown", [tuple([2048] * 128)], 4096, 1536, 128)]
 if len(sys.argv) > 1 and sys.argv[1] == "longk":
@@ -65,8 +68,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "longk":
     cases = [("longk", [(256 * 74,)], 256, 8192, 1)]
 for name, sizes, n, k, G in cases:
     P = Problem(torch, name, sizes, n, k, G, dev, seed=1)
-    for label, flags in [("full", 16), ("nomath", 16 | 1024), ("noprom", 16 | 512), ("neither", 16 | 256 | 512),
-                         ("noload", 16 | 256)]:
+    for label, flags in [("full", 0), ("noprom", 512), ("neither", 256 | 512)]:
         L.tagg_debug_trace(None)
         run(P, flags, G)
         L.tagg_debug_trace(ctypes.c_void_p(buf.data_ptr()))
@@ -74,5 +76,5 @@ for name, sizes, n, k, G in cases:
         run(P, flags, G)
         torch.cuda.synchronize()
         L.tagg_debug_trace(None)
-        report(buf.cpu().numpy(), 8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60, "qdown": 600}[name], f"{name} {label}")
+        report(buf.cpu().numpy(), 8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60, "qdown": 600, "ds": 1000}[name], f"{name} {label}")
     del P
