@@ -115,6 +115,39 @@ int tagg_unpad_rows(const void* c_pad, const int32_t* group_sizes, int G, int N,
                     int64_t m_alloc, void* stream);
 int64_t tagg_padded_rows_bound(int64_t m_alloc, int G);
 
+/* ---- producer side: fused 1x128 quantize + dispatch permutation ---- */
+#define TAGG_DTYPE_BF16 0
+#define TAGG_DTYPE_F32 1
+
+/*
+ * Route plan: a stable counting sort of `rows` routed rows by expert.
+ *   expert_ids   DEVICE int32 [rows], 0 <= id < num_experts (<= 1024)
+ *   group_sizes  DEVICE int32 [num_experts]  <- rows per expert (the GEMM's M_g)
+ *   dest_rows    DEVICE int32 [rows]         <- row of the padding-free grouped layout:
+ *                experts in order, rows of one expert in ascending source order
+ *   workspace    DEVICE int32 [tagg_route_workspace_ints(rows, num_experts)]
+ * Out-of-range ids are skipped and flagged (tagg_route_error).  Stream-ordered,
+ * no host sync.
+ */
+int64_t tagg_route_workspace_ints(int64_t rows, int num_experts);
+int tagg_route_plan(const int32_t* expert_ids, int64_t rows, int num_experts, int32_t* group_sizes,
+                    int32_t* dest_rows, int32_t* workspace, void* stream);
+/* Synchronous read of the route plan's error flag (1 = an expert id out of range). */
+int tagg_route_error(const int32_t* workspace, int64_t rows, int num_experts, int32_t* host_flag);
+
+/*
+ * Fused 1x128 quantization (fp8.py:132-151; encode fp8.py:54-80) and dispatch:
+ * token t's row of x [tokens, K] (bf16 or f32, row stride ldx elements) is quantized
+ * once per 128-column tile, s = fl(amax / 448) (1.0 for an all-zero tile),
+ * code = e4m3(fl(x / s)) RNE saturating, and written to rows dest_rows[t*topk + k],
+ * k < topk (<= 8), of a [*, lda] (codes) and sa [*, ceil(K/128)] (scales).
+ * dest_rows may be NULL with topk == 1 (plain quantize_row_tiles).  Non-finite
+ * inputs set bit 2 of *err_flag (DEVICE int32; the reference raises InvalidInput).
+ */
+int tagg_quantize_dispatch(const void* x, int x_dtype, int64_t ldx, int64_t tokens, int K, int topk,
+                           const int32_t* dest_rows, void* a, int64_t lda, float* sa, int32_t* err_flag,
+                           void* stream);
+
 /* ---- host planners (no GPU needed) ---- */
 /* ProblemConfig validation (engine.py:77-92). */
 int tagg_validate_config(int64_t n, int64_t k, const int64_t* group_sizes, int G, int64_t block_m,

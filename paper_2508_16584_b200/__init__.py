@@ -29,11 +29,19 @@ from .errors import (  # noqa: F401
     CudaError,
     InvalidBlockM,
     InvalidBlockN,
+    InvalidInput,
     NoAlignedSolution,
     ResOutOfRange,
     ShapeMismatch,
     SimError,
     Unsupported,
+)
+from .quant import (  # noqa: F401
+    DispatchedActivations,
+    gather_rows,
+    quantize_dispatch,
+    quantize_row_tiles,
+    route_plan,
 )
 from .planning import (  # noqa: F401
     account,

@@ -1,0 +1,263 @@
+// tagg_quant.cu -- the producer side of the padding-free grouped GEMM (SURVEY.md §8f,
+// rank 1): 1x128 activation quantization fused with the MoE dispatch permutation,
+// writing A / S_A directly in the expert-contiguous, padding-free layout the GEMM
+// consumes (no pad rows, no intermediate copy).
+//
+//   route plan (stable counting sort of the routed rows by expert):
+//     Q1 route_hist_kernel  : per chunk of 1024 rows, per-expert counts
+//     Q2 route_scan_kernel  : chunk x expert exclusive prefix -> chunk bases, group sizes
+//     Q3 route_rank_kernel  : stable rank inside the chunk (warp __match_any) -> dest row
+//   Q4 quantize_dispatch_kernel: one warp per token; per 128-column tile
+//     amax -> s = fl(amax / 448) (1.0 for an all-zero tile) -> codes = e4m3(fl(x / s)),
+//     RNE and saturating (fp8.py:54-80, 132-151); the codes and s go to all topk
+//     destination rows of the token.
+//
+// All kernels are HBM- or latency-bound integer/byte work: 16-byte or 8-byte
+// vector accesses, warp reductions, no tensor cores.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tagg.h"
+
+namespace tagg {
+
+constexpr int kRouteChunk = 1024;  // rows per route chunk (one warp ranks a chunk in order)
+constexpr int kMaxExperts = 1024;
+
+__global__ void __launch_bounds__(256) route_hist_kernel(const int32_t* __restrict__ eid, int64_t R, int E,
+                                                         int32_t* __restrict__ counts, int32_t* __restrict__ err) {
+  __shared__ int32_t h[kMaxExperts];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRouteChunk;
+  for (int i = threadIdx.x; i < kRouteChunk; i += blockDim.x) {
+    const int64_t r = r0 + i;
+    if (r >= R) break;
+    const int e = eid[r];
+    if (e < 0 || e >= E) {
+      atomicOr(err, 1);
+      continue;
+    }
+    atomicAdd(&h[e], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) counts[static_cast<int64_t>(blockIdx.x) * E + i] = h[i];
+}
+
+// One block of up to 1024 threads: thread e walks the chunks of expert e (its column of
+// counts), turning it into an exclusive prefix; a block scan then gives each expert's
+// first row.  base[chunk][e] = first destination row of chunk's rows of expert e.
+__global__ void __launch_bounds__(1024) route_scan_kernel(int32_t* __restrict__ counts, int nchunks, int E,
+                                                          int32_t* __restrict__ group_sizes) {
+  __shared__ int32_t tot[kMaxExperts];
+  __shared__ int32_t warp_sums[32];
+  const int e = threadIdx.x;
+  int run = 0;
+  if (e < E) {
+    for (int c = 0; c < nchunks; ++c) {
+      int32_t* p = counts + static_cast<int64_t>(c) * E + e;
+      const int v = *p;
+      *p = run;
+      run += v;
+    }
+    group_sizes[e] = run;
+  }
+  // exclusive scan of the expert totals
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = (e < E) ? run : 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int s = (lane < static_cast<int>(blockDim.x >> 5)) ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_sums[lane] = s;
+  }
+  __syncthreads();
+  const int excl = x - ((e < E) ? run : 0) + (w > 0 ? warp_sums[w - 1] : 0);
+  if (e < E) tot[e] = excl;
+  __syncthreads();
+  if (e < E)
+    for (int c = 0; c < nchunks; ++c) counts[static_cast<int64_t>(c) * E + e] += tot[e];
+}
+
+// One warp per chunk, 32 rows at a time in order: lanes with the same expert find
+// each other with __match_any_sync; a lane's rank among them plus the chunk's running
+// count for that expert is its stable position.
+__global__ void __launch_bounds__(32) route_rank_kernel(const int32_t* __restrict__ eid, int64_t R, int E,
+                                                        const int32_t* __restrict__ base,
+                                                        int32_t* __restrict__ dest) {
+  __shared__ int32_t run[kMaxExperts];
+  const int lane = threadIdx.x;
+  const int c = blockIdx.x;
+  for (int i = lane; i < E; i += 32) run[i] = base[static_cast<int64_t>(c) * E + i];
+  __syncwarp();
+  const int64_t r0 = static_cast<int64_t>(c) * kRouteChunk;
+  for (int s = 0; s < kRouteChunk; s += 32) {
+    const int64_t r = r0 + s + lane;
+    const bool ok = r < R;
+    int e = ok ? eid[r] : -1;
+    if (e >= E) e = -1;  // invalid ids were flagged by route_hist_kernel
+    const uint32_t same = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(same & ((1u << lane) - 1u));
+    const int leader = __ffs(same) - 1;
+    int pos = 0;
+    if (ok && e >= 0) pos = run[e] + rank;
+    __syncwarp();
+    if (ok && e >= 0) {
+      dest[r] = pos;
+      if (lane == leader) run[e] += __popc(same);
+    }
+    __syncwarp();
+    if (s + 32 >= kRouteChunk || r0 + s + 32 >= R) break;
+  }
+}
+
+// fp8.py:54-80 encode for one f32 pair: RNE, saturating at +-448, -0 keeps its sign.
+__device__ __forceinline__ uint16_t e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+template <bool kBf16>
+__global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __restrict__ x, int64_t ldx, int64_t T,
+                                                                int K, int topk, const int32_t* __restrict__ dest,
+                                                                uint8_t* __restrict__ a, int64_t lda,
+                                                                float* __restrict__ sa, int32_t* __restrict__ err,
+                                                                bool vec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int kb = (K + 127) / 128;
+  int32_t d[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) d[k] = (k < topk) ? (dest ? dest[t * topk + k] : static_cast<int32_t>(t)) : -1;
+  bool bad = false;
+  for (int tile = 0; tile < kb; ++tile) {
+    const int c0 = tile * 128 + 4 * lane;  // this lane's 4 consecutive columns
+    float v[4];
+    if (vec && c0 + 3 < K) {
+      if constexpr (kBf16) {
+        const uint2 raw = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(x) + t * ldx + c0);
+        v[0] = __uint_as_float(raw.x << 16);
+        v[1] = __uint_as_float(raw.x & 0xFFFF0000u);
+        v[2] = __uint_as_float(raw.y << 16);
+        v[3] = __uint_as_float(raw.y & 0xFFFF0000u);
+      } else {
+        const float4 f = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + t * ldx + c0);
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[j] = 0.0f;
+        if (c0 + j < K) {
+          if constexpr (kBf16)
+            v[j] = __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(x)[t * ldx + c0 + j]) << 16);
+          else
+            v[j] = reinterpret_cast<const float*>(x)[t * ldx + c0 + j];
+        }
+      }
+    }
+    float amax = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float m = fabsf(v[j]);
+      bad |= !(m <= 3.402823466e38f);  // inf or nan: the reference raises InvalidInput
+      amax = fmaxf(amax, m);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+    const uint16_t p01 = e4m3x2(__fdiv_rn(v[0], s), __fdiv_rn(v[1], s));
+    const uint16_t p23 = e4m3x2(__fdiv_rn(v[2], s), __fdiv_rn(v[3], s));
+    const uint32_t word = static_cast<uint32_t>(p01) | (static_cast<uint32_t>(p23) << 16);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= topk) break;
+      const int64_t row = d[k];
+      if (vec && c0 + 3 < K) {
+        *reinterpret_cast<uint32_t*>(a + row * lda + c0) = word;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (c0 + j < K) a[row * lda + c0 + j] = static_cast<uint8_t>(word >> (8 * j));
+      }
+      if (lane == 0) sa[row * kb + tile] = s;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 2);
+}
+
+}  // namespace tagg
+
+using namespace tagg;
+
+extern "C" int64_t tagg_route_workspace_ints(int64_t rows, int num_experts) {
+  if (rows < 0 || num_experts < 1) return 0;
+  return ((rows + kRouteChunk - 1) / kRouteChunk) * num_experts + 1;
+}
+
+extern "C" int tagg_route_plan(const int32_t* expert_ids, int64_t rows, int num_experts, int32_t* group_sizes,
+                               int32_t* dest_rows, int32_t* workspace, void* stream) {
+  if (rows < 0 || num_experts < 1 || num_experts > kMaxExperts) return TAGG_ERR_CONFIG;
+  if (!group_sizes || !workspace || (rows > 0 && (!expert_ids || !dest_rows))) return TAGG_ERR_SHAPE;
+  if (rows >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nchunks = static_cast<int>((rows + kRouteChunk - 1) / kRouteChunk);
+  int32_t* err = workspace + static_cast<int64_t>(nchunks) * num_experts;
+  if (cudaMemsetAsync(err, 0, sizeof(int32_t), st) != cudaSuccess) return TAGG_ERR_CUDA;
+  if (nchunks == 0) {
+    return cudaMemsetAsync(group_sizes, 0, sizeof(int32_t) * num_experts, st) == cudaSuccess ? TAGG_OK
+                                                                                           : TAGG_ERR_CUDA;
+  }
+  route_hist_kernel<<<nchunks, 256, 0, st>>>(expert_ids, rows, num_experts, workspace, err);
+  route_scan_kernel<<<1, 1024, 0, st>>>(workspace, nchunks, num_experts, group_sizes);
+  route_rank_kernel<<<nchunks, 32, 0, st>>>(expert_ids, rows, num_experts, workspace, dest_rows);
+  return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
+}
+
+extern "C" int tagg_route_error(const int32_t* workspace, int64_t rows, int num_experts, int32_t* host_flag) {
+  if (!workspace || !host_flag || num_experts < 1) return TAGG_ERR_SHAPE;
+  const int64_t nchunks = (rows + kRouteChunk - 1) / kRouteChunk;
+  return cudaMemcpy(host_flag, workspace + nchunks * num_experts, sizeof(int32_t), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess
+             ? TAGG_OK
+             : TAGG_ERR_CUDA;
+}
+
+extern "C" int tagg_quantize_dispatch(const void* x, int x_dtype, int64_t ldx, int64_t tokens, int K, int topk,
+                                      const int32_t* dest_rows, void* a, int64_t lda, float* sa, int32_t* err_flag,
+                                      void* stream) {
+  if (K < 1 || tokens < 0 || topk < 1 || topk > 8) return TAGG_ERR_CONFIG;
+  if (x_dtype != TAGG_DTYPE_BF16 && x_dtype != TAGG_DTYPE_F32) return TAGG_ERR_CONFIG;
+  if (ldx < K || lda < K) return TAGG_ERR_SHAPE;
+  if (tokens == 0) return TAGG_OK;
+  if (!x || !a || !sa || !err_flag || (topk > 1 && !dest_rows)) return TAGG_ERR_SHAPE;
+  const int esz = x_dtype == TAGG_DTYPE_BF16 ? 2 : 4;
+  // vector path: 8 B (bf16) / 16 B (f32) loads at column multiples of 4 and 4-byte code
+  // stores; any other alignment takes the element-wise path
+  const bool vec = !(reinterpret_cast<uintptr_t>(x) % (4 * esz)) && !((ldx * esz) % (4 * esz)) &&
+                   !(reinterpret_cast<uintptr_t>(a) % 4) && !(lda % 4);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int warps = 8;
+  const int64_t blocks = (tokens + warps - 1) / warps;
+  if (blocks >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
+  if (x_dtype == TAGG_DTYPE_BF16)
+    quantize_dispatch_kernel<true><<<static_cast<unsigned>(blocks), 32 * warps, 0, st>>>(
+        x, ldx, tokens, K, topk, dest_rows, static_cast<uint8_t*>(a), lda, sa, err_flag, vec);
+  else
+    quantize_dispatch_kernel<false><<<static_cast<unsigned>(blocks), 32 * warps, 0, st>>>(
+        x, ldx, tokens, K, topk, dest_rows, static_cast<uint8_t*>(a), lda, sa, err_flag, vec);
+  return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
+}
