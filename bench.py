@@ -504,7 +504,35 @@ def run_extra(torch, tg, dev, rank, fp8_peak, exact):
                      "memory_saved_pct": acc.saving_pct, "ms": ms["adaptive"]}
         del P
         torch.cuda.empty_cache()
+    out["quantize_dispatch_dsv3"] = run_quantize_dispatch(torch, tg, dev)
     return out
+
+
+def run_quantize_dispatch(torch, tg, dev, tokens=32768, k=7168, topk=8, experts=256, iters=10, warmup=3):
+    """bf16 activations -> 1x128 FP8 codes + scales written straight
+    into the expert-contiguous padding-free layout (route plan + fused quantize/scatter).
+    HBM-bound: algorithmic bytes = x read + codes/scales/dest written + routing ids."""
+    gen = torch.Generator(device=dev).manual_seed(3)
+    x = torch.randn((tokens, k), device=dev, generator=gen).to(torch.bfloat16)
+    logits = torch.randn((tokens, experts), device=dev, generator=gen)
+    eids = torch.topk(logits, topk, dim=1).indices.to(torch.int32)
+    for _ in range(warmup):
+        tg.quantize_dispatch(x, eids, experts)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        tg.quantize_dispatch(x, eids, experts)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / iters
+    kb = -(-k // 128)
+    rows = tokens * topk
+    nbytes = tokens * k * 2 + rows * 4 + rows * (k + 4 * kb) + rows * 4 + experts * 4
+    peak = _peaks()[0]["hbm_gbs"]
+    return {"tokens": tokens, "K": k, "topk": topk, "experts": experts, "ms": ms,
+            "algorithmic_bytes": nbytes, "gbs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / peak,
+            "hbm_peak_gbs": peak, "note": "route plan (3 launches) + quantize/scatter (1 launch), x resident"}
 
 
 def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, warmup=2):

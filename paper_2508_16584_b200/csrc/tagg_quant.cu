@@ -143,25 +143,37 @@ __global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __re
 #pragma unroll
   for (int k = 0; k < 8; ++k) d[k] = (k < topk) ? (dest ? dest[t * topk + k] : static_cast<int32_t>(t)) : -1;
   bool bad = false;
-  for (int tile = 0; tile < kb; ++tile) {
-    const int c0 = tile * 128 + 4 * lane;  // this lane's 4 consecutive columns
-    float v[4];
-    if (vec && c0 + 3 < K) {
+  // A warp covers 4 tiles per step: lane l holds 16 consecutive columns of tile
+  // 4 step + l / 8 (8 lanes per 128-column tile): 32-B loads, 16-B code stores.
+  const int sub = lane >> 3, part = lane & 7;
+  for (int tile0 = 0; tile0 < kb; tile0 += 4) {
+    const int tile = tile0 + sub;
+    const int c0 = tile * 128 + 16 * part;
+    float v[16];
+    const bool full16 = vec && c0 + 15 < K;
+    if (full16) {
       if constexpr (kBf16) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(x) + t * ldx + c0);
-        v[0] = __uint_as_float(raw.x << 16);
-        v[1] = __uint_as_float(raw.x & 0xFFFF0000u);
-        v[2] = __uint_as_float(raw.y << 16);
-        v[3] = __uint_as_float(raw.y & 0xFFFF0000u);
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + t * ldx + c0);
+        const uint4 r0 = src[0], r1 = src[1];
+        const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[2 * j] = __uint_as_float(w[j] << 16);
+          v[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+        }
       } else {
-        const float4 f = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + t * ldx + c0);
-        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + t * ldx + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 f = src[j];
+          v[4 * j] = f.x; v[4 * j + 1] = f.y; v[4 * j + 2] = f.z; v[4 * j + 3] = f.w;
+        }
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 16; ++j) {
         v[j] = 0.0f;
-        if (c0 + j < K) {
+        if (tile < kb && c0 + j < K) {
           if constexpr (kBf16)
             v[j] = __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(x)[t * ldx + c0 + j]) << 16);
           else
@@ -171,29 +183,35 @@ __global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __re
     }
     float amax = 0.0f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 16; ++j) {
       const float m = fabsf(v[j]);
       bad |= !(m <= 3.402823466e38f);  // inf or nan: the reference raises InvalidInput
       amax = fmaxf(amax, m);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    for (int o = 4; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
-    const uint16_t p01 = e4m3x2(__fdiv_rn(v[0], s), __fdiv_rn(v[1], s));
-    const uint16_t p23 = e4m3x2(__fdiv_rn(v[2], s), __fdiv_rn(v[3], s));
-    const uint32_t word = static_cast<uint32_t>(p01) | (static_cast<uint32_t>(p23) << 16);
+    uint32_t word[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (k >= topk) break;
-      const int64_t row = d[k];
-      if (vec && c0 + 3 < K) {
-        *reinterpret_cast<uint32_t*>(a + row * lda + c0) = word;
-      } else {
+    for (int j = 0; j < 4; ++j) {
+      const uint16_t lo = e4m3x2(__fdiv_rn(v[4 * j], s), __fdiv_rn(v[4 * j + 1], s));
+      const uint16_t hi = e4m3x2(__fdiv_rn(v[4 * j + 2], s), __fdiv_rn(v[4 * j + 3], s));
+      word[j] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    }
+    if (tile < kb) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (c0 + j < K) a[row * lda + c0 + j] = static_cast<uint8_t>(word >> (8 * j));
+      for (int k = 0; k < 8; ++k) {
+        if (k >= topk) break;
+        const int64_t row = d[k];
+        if (full16) {
+          *reinterpret_cast<uint4*>(a + row * lda + c0) = make_uint4(word[0], word[1], word[2], word[3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < K) a[row * lda + c0 + j] = static_cast<uint8_t>(word[j >> 2] >> (8 * (j & 3)));
+        }
+        if (part == 0) sa[row * kb + tile] = s;
       }
-      if (lane == 0) sa[row * kb + tile] = s;
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 2);
@@ -245,10 +263,10 @@ extern "C" int tagg_quantize_dispatch(const void* x, int x_dtype, int64_t ldx, i
   if (tokens == 0) return TAGG_OK;
   if (!x || !a || !sa || !err_flag || (topk > 1 && !dest_rows)) return TAGG_ERR_SHAPE;
   const int esz = x_dtype == TAGG_DTYPE_BF16 ? 2 : 4;
-  // vector path: 8 B (bf16) / 16 B (f32) loads at column multiples of 4 and 4-byte code
-  // stores; any other alignment takes the element-wise path
-  const bool vec = !(reinterpret_cast<uintptr_t>(x) % (4 * esz)) && !((ldx * esz) % (4 * esz)) &&
-                   !(reinterpret_cast<uintptr_t>(a) % 4) && !(lda % 4);
+  // vector path: 16-byte loads and 16-byte code stores at column multiples of 16;
+  // any other alignment takes the element-wise path
+  const bool vec = !(reinterpret_cast<uintptr_t>(x) % 16) && !((ldx * esz) % 16) &&
+                   !(reinterpret_cast<uintptr_t>(a) % 16) && !(lda % 16);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int warps = 8;
   const int64_t blocks = (tokens + warps - 1) / warps;
