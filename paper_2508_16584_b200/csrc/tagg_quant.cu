@@ -5,8 +5,9 @@
 //
 //   route plan (stable counting sort of the routed rows by expert):
 //     Q1 route_hist_kernel  : per chunk of 1024 rows, per-expert counts
-//     Q2 route_scan_kernel  : chunk x expert exclusive prefix -> chunk bases, group sizes
-//     Q3 route_rank_kernel  : stable rank inside the chunk (warp __match_any) -> dest row
+//     Q2 route_scan_kernel  : per expert, exclusive prefix over chunks; group sizes
+//     Q3 route_rank_kernel  : expert offsets + stable rank inside the chunk
+//                             (warp __match_any) -> dest row
 //   Q4 quantize_dispatch_kernel: one warp per token; per 128-column tile
 //     amax -> s = fl(amax / 448) (1.0 for an all-zero tile) -> codes = e4m3(fl(x / s)),
 //     RNE and saturating (fp8.py:54-80, 132-151); the codes and s go to all topk
@@ -42,52 +43,39 @@ __global__ void __launch_bounds__(256) route_hist_kernel(const int32_t* __restri
     atomicAdd(&h[e], 1);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < E; i += blockDim.x) counts[static_cast<int64_t>(blockIdx.x) * E + i] = h[i];
+  // expert-major [E][nchunks]: the per-expert scan reads a contiguous column
+  for (int i = threadIdx.x; i < E; i += blockDim.x) counts[static_cast<int64_t>(i) * gridDim.x + blockIdx.x] = h[i];
 }
 
-// One block of up to 1024 threads: thread e walks the chunks of expert e (its column of
-// counts), turning it into an exclusive prefix; a block scan then gives each expert's
-// first row.  base[chunk][e] = first destination row of chunk's rows of expert e.
-__global__ void __launch_bounds__(1024) route_scan_kernel(int32_t* __restrict__ counts, int nchunks, int E,
-                                                          int32_t* __restrict__ group_sizes) {
-  __shared__ int32_t tot[kMaxExperts];
-  __shared__ int32_t warp_sums[32];
-  const int e = threadIdx.x;
-  int run = 0;
-  if (e < E) {
-    for (int c = 0; c < nchunks; ++c) {
-      int32_t* p = counts + static_cast<int64_t>(c) * E + e;
-      const int v = *p;
-      *p = run;
-      run += v;
-    }
-    group_sizes[e] = run;
-  }
-  // exclusive scan of the expert totals
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int x = (e < E) ? run : 0;
+// One warp per expert: lane l owns chunks [l*cpl, (l+1)*cpl) of the expert's contiguous
+// count column; a warp scan of the lane sums gives each lane's starting offset and the
+// column becomes an exclusive prefix (the expert's rows before each chunk).
+// group_sizes[e] = the expert's total.
+__global__ void __launch_bounds__(256) route_scan_kernel(int32_t* __restrict__ counts, int nchunks, int E,
+                                                         int32_t* __restrict__ group_sizes) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (e >= E) return;
+  int32_t* col = counts + static_cast<int64_t>(e) * nchunks;
+  const int cpl = (nchunks + 31) / 32;
+  const int c0 = min(nchunks, lane * cpl), c1 = min(nchunks, c0 + cpl);
+  int sum = 0;
+#pragma unroll 8
+  for (int c = c0; c < c1; ++c) sum += col[c];
+  int incl = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
-  if (lane == 31) warp_sums[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int s = (lane < static_cast<int>(blockDim.x >> 5)) ? warp_sums[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    warp_sums[lane] = s;
+  int run = incl - sum;
+#pragma unroll 8
+  for (int c = c0; c < c1; ++c) {
+    const int v = col[c];
+    col[c] = run;
+    run += v;
   }
-  __syncthreads();
-  const int excl = x - ((e < E) ? run : 0) + (w > 0 ? warp_sums[w - 1] : 0);
-  if (e < E) tot[e] = excl;
-  __syncthreads();
-  if (e < E)
-    for (int c = 0; c < nchunks; ++c) counts[static_cast<int64_t>(c) * E + e] += tot[e];
+  if (lane == 31) group_sizes[e] = incl;
 }
 
 // One warp per chunk, 32 rows at a time in order: lanes with the same expert find
@@ -95,11 +83,29 @@ __global__ void __launch_bounds__(1024) route_scan_kernel(int32_t* __restrict__ 
 // count for that expert is its stable position.
 __global__ void __launch_bounds__(32) route_rank_kernel(const int32_t* __restrict__ eid, int64_t R, int E,
                                                         const int32_t* __restrict__ base,
+                                                        const int32_t* __restrict__ group_sizes,
                                                         int32_t* __restrict__ dest) {
   __shared__ int32_t run[kMaxExperts];
   const int lane = threadIdx.x;
   const int c = blockIdx.x;
-  for (int i = lane; i < E; i += 32) run[i] = base[static_cast<int64_t>(c) * E + i];
+  // expert offsets: exclusive scan of the group sizes (lane l sums experts [l*epl, (l+1)*epl))
+  {
+    const int epl = (E + 31) / 32;
+    const int e0 = min(E, lane * epl), e1 = min(E, e0 + epl);
+    int sum = 0;
+    for (int e = e0; e < e1; ++e) sum += group_sizes[e];
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int off = incl - sum;
+    for (int e = e0; e < e1; ++e) {
+      run[e] = off + base[static_cast<int64_t>(e) * gridDim.x + c];
+      off += group_sizes[e];
+    }
+  }
   __syncwarp();
   const int64_t r0 = static_cast<int64_t>(c) * kRouteChunk;
   for (int s = 0; s < kRouteChunk; s += 32) {
@@ -240,8 +246,8 @@ extern "C" int tagg_route_plan(const int32_t* expert_ids, int64_t rows, int num_
                                                                                            : TAGG_ERR_CUDA;
   }
   route_hist_kernel<<<nchunks, 256, 0, st>>>(expert_ids, rows, num_experts, workspace, err);
-  route_scan_kernel<<<1, 1024, 0, st>>>(workspace, nchunks, num_experts, group_sizes);
-  route_rank_kernel<<<nchunks, 32, 0, st>>>(expert_ids, rows, num_experts, workspace, dest_rows);
+  route_scan_kernel<<<(num_experts + 7) / 8, 256, 0, st>>>(workspace, nchunks, num_experts, group_sizes);
+  route_rank_kernel<<<nchunks, 32, 0, st>>>(expert_ids, rows, num_experts, workspace, group_sizes, dest_rows);
   return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
 }
 
