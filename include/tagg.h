@@ -148,6 +148,17 @@ int tagg_quantize_dispatch(const void* x, int x_dtype, int64_t ldx, int64_t toke
                            const int32_t* dest_rows, void* a, int64_t lda, float* sa, int32_t* err_flag,
                            void* stream);
 
+/*
+ * 128x128 block quantization (fp8.py:154-176), batched: matrix b of x (rows x cols,
+ * row stride ldx, matrix stride x_batch_stride elements) -> codes (row stride ldc,
+ * matrix stride codes_batch_stride bytes) and scales [batch][ceil(rows/128)][ceil(cols/128)].
+ * One scale per block, s = fl(amax / 448) (1.0 for an all-zero block), codes as in
+ * tagg_quantize_dispatch.  Per-expert weights [G, K, N] are batch = G, rows = K, cols = N.
+ */
+int tagg_quantize_blocks(const void* x, int x_dtype, int64_t batch, int64_t rows, int64_t cols, int64_t ldx,
+                         int64_t x_batch_stride, void* codes, int64_t ldc, int64_t codes_batch_stride,
+                         float* scales, int32_t* err_flag, void* stream);
+
 /* ---- host planners (no GPU needed) ---- */
 /* ProblemConfig validation (engine.py:77-92). */
 int tagg_validate_config(int64_t n, int64_t k, const int64_t* group_sizes, int G, int64_t block_m,

@@ -39,6 +39,7 @@ from .errors import (  # noqa: F401
 from .quant import (  # noqa: F401
     DispatchedActivations,
     gather_rows,
+    quantize_blocks,
     quantize_dispatch,
     quantize_row_tiles,
     route_plan,

@@ -223,9 +223,94 @@ __global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __re
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 2);
 }
 
+// fp8.py:154-176: one scale per 128x128 block.  One CTA per block (grid: column
+// blocks x row blocks x batch), 8 warps x 16 rows, 4 columns per lane: 64 values per
+// thread held in registers across the block-wide amax.
+template <bool kBf16>
+__global__ void __launch_bounds__(256) quantize_blocks_kernel(const void* __restrict__ x, int64_t ldx,
+                                                              int64_t batch_stride, int rows, int cols,
+                                                              uint8_t* __restrict__ codes, int64_t ldc,
+                                                              int64_t codes_batch_stride, float* __restrict__ scales,
+                                                              int32_t* __restrict__ err) {
+  __shared__ float wmax[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cb = gridDim.x, rb = gridDim.y;
+  const int c = blockIdx.x * 128 + 4 * lane;
+  const int r0 = blockIdx.y * 128 + 16 * w;
+  const int64_t bx = static_cast<int64_t>(blockIdx.z) * batch_stride;
+  float v[16][4];
+  float amax = 0.0f;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = r0 + i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float f = 0.0f;
+      if (r < rows && c + j < cols) {
+        const int64_t idx = bx + static_cast<int64_t>(r) * ldx + c + j;
+        if constexpr (kBf16)
+          f = __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(x)[idx]) << 16);
+        else
+          f = reinterpret_cast<const float*>(x)[idx];
+      }
+      v[i][j] = f;
+      const float m = fabsf(f);
+      bad |= !(m <= 3.402823466e38f);
+      amax = fmaxf(amax, m);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (lane == 0) wmax[w] = amax;
+  __syncthreads();
+  amax = wmax[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) amax = fmaxf(amax, wmax[i]);
+  const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  const int64_t cbase = static_cast<int64_t>(blockIdx.z) * codes_batch_stride;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = r0 + i;
+    if (r >= rows) break;
+    const uint16_t lo = e4m3x2(__fdiv_rn(v[i][0], s), __fdiv_rn(v[i][1], s));
+    const uint16_t hi = e4m3x2(__fdiv_rn(v[i][2], s), __fdiv_rn(v[i][3], s));
+    const uint32_t word = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    uint8_t* dst = codes + cbase + static_cast<int64_t>(r) * ldc + c;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (c + j < cols) dst[j] = static_cast<uint8_t>(word >> (8 * j));
+  }
+  if (threadIdx.x == 0)
+    scales[(static_cast<int64_t>(blockIdx.z) * rb + blockIdx.y) * cb + blockIdx.x] = s;
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 2);
+}
+
 }  // namespace tagg
 
 using namespace tagg;
+
+extern "C" int tagg_quantize_blocks(const void* x, int x_dtype, int64_t batch, int64_t rows, int64_t cols,
+                                    int64_t ldx, int64_t x_batch_stride, void* codes, int64_t ldc,
+                                    int64_t codes_batch_stride, float* scales, int32_t* err_flag, void* stream) {
+  if (x_dtype != TAGG_DTYPE_BF16 && x_dtype != TAGG_DTYPE_F32) return TAGG_ERR_CONFIG;
+  if (batch < 0 || rows < 0 || cols < 0 || ldx < cols || ldc < cols) return TAGG_ERR_SHAPE;
+  if (batch == 0 || rows == 0 || cols == 0) return TAGG_OK;
+  if (!x || !codes || !scales || !err_flag) return TAGG_ERR_SHAPE;
+  const int64_t rb = (rows + 127) / 128, cb = (cols + 127) / 128;
+  if (rb > 65535 || batch > 65535 || cb >= (int64_t(1) << 31) || rows >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 grid(static_cast<unsigned>(cb), static_cast<unsigned>(rb), static_cast<unsigned>(batch));
+  if (x_dtype == TAGG_DTYPE_BF16)
+    quantize_blocks_kernel<true><<<grid, 256, 0, st>>>(x, ldx, x_batch_stride, static_cast<int>(rows),
+                                                       static_cast<int>(cols), static_cast<uint8_t*>(codes), ldc,
+                                                       codes_batch_stride, scales, err_flag);
+  else
+    quantize_blocks_kernel<false><<<grid, 256, 0, st>>>(x, ldx, x_batch_stride, static_cast<int>(rows),
+                                                        static_cast<int>(cols), static_cast<uint8_t*>(codes), ldc,
+                                                        codes_batch_stride, scales, err_flag);
+  return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
+}
 
 extern "C" int64_t tagg_route_workspace_ints(int64_t rows, int num_experts) {
   if (rows < 0 || num_experts < 1) return 0;

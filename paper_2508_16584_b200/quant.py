@@ -93,6 +93,38 @@ def quantize_row_tiles(x: torch.Tensor, *, check: bool = False):
     return _quantize(x, 1, None, x.shape[0], check)
 
 
+def quantize_blocks(w: torch.Tensor, *, check: bool = False):
+    """fp8.py:154-176 on the GPU, batched over leading dims: one scale per 128x128 block.
+
+    w: [..., rows, cols] bf16/f32 (e.g. per-expert weights [G, K, N]).  Returns
+    (codes uint8 of w's shape, scales f32 [..., ceil(rows/128), ceil(cols/128)]),
+    bit-identical to the reference for finite input.
+    """
+    _check_cuda(w, "w")
+    if w.dim() < 2:
+        raise InvalidInput("expected a matrix or a batch of matrices")
+    if w.dtype not in _DTYPES:
+        w = w.to(torch.float32)
+    lead = w.shape[:-2]
+    rows, cols = w.shape[-2:]
+    w3 = w.reshape(-1, rows, cols)
+    if w3.stride(-1) != 1:
+        w3 = w3.contiguous()
+    batch = w3.shape[0]
+    rb, cb = -(-rows // 128), -(-cols // 128)
+    codes = torch.empty((batch, rows, cols), dtype=torch.uint8, device=w.device)
+    scales = torch.empty((batch, rb, cb), dtype=torch.float32, device=w.device)
+    err = torch.zeros(1, dtype=torch.int32, device=w.device)
+    if batch and rows and cols:
+        rc = lib().tagg_quantize_blocks(w3.data_ptr(), _DTYPES[w3.dtype], batch, rows, cols, w3.stride(1),
+                                        w3.stride(0), codes.data_ptr(), cols, rows * cols, scales.data_ptr(),
+                                        err.data_ptr(), _stream())
+        raise_for_status(rc, "tagg_quantize_blocks")
+    if check and int(err.item()):
+        raise InvalidInput("matrix entries must be finite")
+    return codes.view(*lead, rows, cols), scales.view(*lead, rb, cb)
+
+
 @dataclass
 class DispatchedActivations:
     """Quantized activations in the padding-free grouped layout."""

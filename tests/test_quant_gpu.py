@@ -114,3 +114,24 @@ def test_quantize_dispatch_feeds_the_grouped_gemm(dtype):
     assert back.shape == (tokens, topk, n)
     np.testing.assert_array_equal(back[5, 2].view(torch.int16).cpu().numpy(),
                                   c[int(d.dest_rows[5 * topk + 2])].view(torch.int16).cpu().numpy())
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (128, 128), (200, 300), (3, 256, 384), (2, 7168, 4096)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_quantize_blocks_is_bit_exact(shape, dtype):
+    """fp8.py:154-176 per matrix of the batch (per-expert weights [G, K, N])."""
+    rng = np.random.Generator(np.random.PCG64(sum(shape)))
+    w = rng.standard_normal(shape).astype(np.float32) * np.exp2(rng.integers(-6, 6, size=shape[:-1] + (1,)))
+    w = w.astype(np.float32)
+    if w.ndim == 3 and w.shape[0] > 1:
+        w[1, :128, :128] = 0.0  # an all-zero block: scale 1.0
+    wt = torch.from_numpy(w).to(DEV).to(dtype)
+    codes, scales = tg.quantize_blocks(wt, check=True)
+    torch.cuda.synchronize()
+    ref = wt.float().cpu().numpy().reshape((-1,) + shape[-2:])
+    got_c = codes.cpu().numpy().reshape((-1,) + shape[-2:])
+    got_s = scales.cpu().numpy().reshape((ref.shape[0],) + scales.shape[-2:])
+    for b in range(ref.shape[0]):
+        want_c, want_s = ofp8.quantize_blocks(ref[b])
+        np.testing.assert_array_equal(got_c[b], want_c)
+        np.testing.assert_array_equal(got_s[b].view(np.uint32), want_s.view(np.uint32))
