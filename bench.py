@@ -421,11 +421,18 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
 
     # ---------------------------------------------------------------- other BASELINE configs
+    # secondary lines never cost the headline: a failure is recorded, not raised
     extra = {}
     if not args.no_extra:
-        extra = run_extra(torch, tg, dev, rank, fp8_peak, args.exact)
+        try:
+            extra = run_extra(torch, tg, dev, rank, fp8_peak, args.exact)
+        except Exception as exc:  # noqa: BLE001
+            extra = {"error": f"{type(exc).__name__}: {exc}"}
     if world > 1:
-        extra["deepseek_v3_down_ep"] = run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, args.exact)
+        try:
+            extra["deepseek_v3_down_ep"] = run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, args.exact)
+        except Exception as exc:  # noqa: BLE001
+            extra["deepseek_v3_down_ep"] = {"error": f"{type(exc).__name__}: {exc}"}
 
     if rank != 0:
         if world > 1:
