@@ -58,4 +58,6 @@ from .planning import (  # noqa: F401
     window_rows,
 )
 
+from . import ops  # noqa: F401,E402  (registers torch.ops.tagg.*)
+
 __version__ = "0.1.0"

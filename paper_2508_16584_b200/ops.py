@@ -1,0 +1,61 @@
+"""torch.ops.tagg.* -- the grouped GEMM and the producer kernels as PyTorch operators
+(SURVEY.md §8b, item 2).
+
+Registered with torch.library for the CUDA device type only: there is no CPU kernel,
+so a CPU tensor raises instead of silently falling back.  Each op has a fake
+(meta) implementation, so the ops trace under torch.compile / FakeTensor and can
+sit inside captured graphs.  The CUDA implementations call libtagg.so through
+the C ABI, stream-ordered on the current stream, with no host sync.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import engine, quant
+
+_LIB = "tagg"
+
+
+@torch.library.custom_op(f"{_LIB}::grouped_gemm_fp8", mutates_args=(), device_types="cuda")
+def grouped_gemm_fp8(a: torch.Tensor, a_scales: torch.Tensor, b: torch.Tensor, b_scales: torch.Tensor,
+                     group_sizes: torch.Tensor, b_layout: str = "kn", exact_promotion: bool = False) -> torch.Tensor:
+    """Padding-free FP8 grouped GEMM -> bf16 [m_alloc, N] (rows past sum(M_g) are unspecified)."""
+    return engine.grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, b_layout=b_layout,
+                                   exact_promotion=exact_promotion)
+
+
+@grouped_gemm_fp8.register_fake
+def _(a, a_scales, b, b_scales, group_sizes, b_layout="kn", exact_promotion=False):
+    n = b.shape[-1] if b_layout == "kn" else b.shape[-2]
+    return a.new_empty((a.shape[0], n), dtype=torch.bfloat16)
+
+
+@torch.library.custom_op(f"{_LIB}::quantize_row_tiles", mutates_args=(), device_types="cuda")
+def quantize_row_tiles(x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """fp8.py:132-151: (codes uint8 [rows, K], scales f32 [rows, ceil(K/128)])."""
+    codes, scales = quant.quantize_row_tiles(x)
+    return codes.contiguous(), scales
+
+
+@quantize_row_tiles.register_fake
+def _(x):
+    k = x.shape[1]
+    return x.new_empty((x.shape[0], k), dtype=torch.uint8), x.new_empty((x.shape[0], -(-k // 128)),
+                                                                        dtype=torch.float32)
+
+
+@torch.library.custom_op(f"{_LIB}::quantize_dispatch", mutates_args=(), device_types="cuda")
+def quantize_dispatch(x: torch.Tensor, expert_ids: torch.Tensor,
+                      num_experts: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Fused 1x128 quantize + dispatch: (a_codes, a_scales, group_sizes, dest_rows)."""
+    d = quant.quantize_dispatch(x, expert_ids, num_experts)
+    return d.a_codes.contiguous(), d.a_scales, d.group_sizes, d.dest_rows
+
+
+@quantize_dispatch.register_fake
+def _(x, expert_ids, num_experts):
+    t, k = x.shape
+    rows = expert_ids.numel()
+    return (x.new_empty((rows, k), dtype=torch.uint8), x.new_empty((rows, -(-k // 128)), dtype=torch.float32),
+            x.new_empty((num_experts,), dtype=torch.int32), x.new_empty((rows,), dtype=torch.int32))
