@@ -68,6 +68,35 @@ def dispatch(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_ids: torch.Te
     a_sorted = a_codes.index_select(0, order)
     sa_sorted = a_scales.index_select(0, order)
     counts = _counts(expert_ids, num_experts)                       # [E] rows per expert, local
+    return _exchange(a_sorted, sa_sorted, counts, order, epr, group)
+
+
+def dispatch_tokens(x: torch.Tensor, expert_ids: torch.Tensor, num_experts: int, group=None):
+    """Quantize-and-dispatch from bf16/f32 activations (SURVEY.md §8f ranks 1+3).
+
+    x [T, K] activations, expert_ids [T, topk].  The fused kernel (quant.quantize_dispatch)
+    quantizes every token once (1x128, fp8.py:132-151) and writes its topk rows already in
+    expert order, so the local sort of dispatch() disappears; the rows then go through the
+    same all-to-all.  Returns (a_local, sa_local, meta) like dispatch(); combine() inverts it
+    back to (token, k) rows.
+    """
+    from . import quant
+
+    world = dist.get_world_size(group)
+    if num_experts % world:
+        raise ValueError(f"{num_experts} experts do not split over {world} ranks")
+    d = quant.quantize_dispatch(x, expert_ids, num_experts)
+    order = torch.empty_like(d.dest_rows, dtype=torch.int64)       # sorted row -> local (t, k) row
+    order[d.dest_rows.to(torch.int64)] = torch.arange(d.dest_rows.numel(), device=x.device)
+    return _exchange(d.a_codes.contiguous(), d.a_scales, d.group_sizes, order, num_experts // world, group)
+
+
+def _exchange(a_sorted, sa_sorted, counts, order, epr, group):
+    """All-to-all of expert-sorted local rows; regroup received rows to expert-contiguous."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = a_sorted.device
+    a_codes, a_scales = a_sorted, sa_sorted
     recv_counts = torch.empty_like(counts)                          # [P * epr] from each source
     dist.all_to_all_single(recv_counts, counts, group=group)
     send_splits = counts.view(world, epr).sum(1)

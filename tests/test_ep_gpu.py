@@ -1,0 +1,48 @@
+"""EP dispatch on the GPU with NCCL (world size 1 in-process; the multi-rank logic is
+covered by tests/test_ep_gloo.py): the fused quantize-and-dispatch path equals
+quantizing first and dispatching the FP8 rows, and combine() returns every row home."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import paper_2508_16584_b200 as tg
+from paper_2508_16584_b200 import ep
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl1():
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29613")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+def test_dispatch_tokens_equals_quantize_then_dispatch(nccl1):
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(9)
+    tokens, topk, experts, k = 500, 4, 16, 384
+    x = torch.randn((tokens, k), device=dev, generator=g).to(torch.bfloat16)
+    eids = torch.topk(torch.rand((tokens, experts), device=dev, generator=g), topk, dim=1).indices.to(torch.int32)
+    a1, sa1, m1 = ep.dispatch_tokens(x, eids, experts)
+    codes, scales = tg.quantize_row_tiles(x)
+    rows_codes = codes.repeat_interleave(topk, dim=0)                # local (t, k) rows
+    rows_scales = scales.repeat_interleave(topk, dim=0)
+    a2, sa2, m2 = ep.dispatch(rows_codes, rows_scales, eids.reshape(-1), experts)
+    torch.cuda.synchronize()
+    assert torch.equal(a1, a2) and torch.equal(sa1, sa2)
+    assert torch.equal(m1.group_sizes, m2.group_sizes)
+    # combine returns each grouped row to its (token, k) slot
+    c = a1.to(torch.float32)[:, :8]
+    back = ep.combine(c, m1)
+    want = rows_codes.to(torch.float32)[:, :8]
+    assert np.array_equal(back.cpu().numpy(), want.cpu().numpy())
