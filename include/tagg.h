@@ -159,6 +159,29 @@ int tagg_quantize_blocks(const void* x, int x_dtype, int64_t batch, int64_t rows
                          int64_t x_batch_stride, void* codes, int64_t ldc, int64_t codes_batch_stride,
                          float* scales, int32_t* err_flag, void* stream);
 
+/* ---- backward: weight gradient as a K-grouped GEMM ---- */
+/*
+ * Per-group 128x1 quantization for the weight gradient: for every group's 128-token
+ * block and column c, s = fl(amax / 448) (1.0 when zero) over the block's rows (fewer
+ * than 128 in a group's last block) and codes = e4m3(fl(x / s)).  codes [m_alloc, cols]
+ * (row stride ldc), scales [tagg_token_blocks_bound(m_alloc, G), cols] of which the
+ * first sum(ceil(M_g/128)) rows are written, group by group.  group_sizes on the device.
+ */
+int64_t tagg_token_blocks_bound(int64_t m_alloc, int G);
+int tagg_quantize_col_blocks(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
+                             const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
+                             int32_t* err_flag, void* stream);
+/*
+ * dW_g = X_g^T dY_g for every group (K % 128 == 0, N % 128 == 0): x [m_alloc, K] and
+ * dy [m_alloc, N] e4m3 codes in the padding-free grouped layout (dense rows), sx [TB, K]
+ * and sdy [TB, N] from tagg_quantize_col_blocks, dw bf16 [G, K, N].  The ragged M_g is the
+ * reduction axis: a group's last token block is loaded with the power-of-two TMA
+ * descriptor pool in two phases and the rows past the group end are zeroed in smem, so
+ * no other group's token enters the sum.  An empty group gets dW = 0.
+ */
+int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, const float* sdy, int64_t m_alloc,
+                   const int32_t* group_sizes, int G, int K, int N, void* dw, void* stream);
+
 /* ---- host planners (no GPU needed) ---- */
 /* ProblemConfig validation (engine.py:77-92). */
 int tagg_validate_config(int64_t n, int64_t k, const int64_t* group_sizes, int G, int64_t block_m,

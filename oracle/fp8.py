@@ -98,3 +98,28 @@ def bf16_bits_to_f32(bits) -> np.ndarray:
     """engine.py:53-55"""
     u = np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)
     return u.view(np.float32)
+
+
+def quantize_col_blocks(x, group_sizes):
+    """Per-group 128x1 quantization for the weight gradient (the ragged token axis is the
+    reduction axis): for each group and each of its 128-token blocks, one scale per
+    column, s = fl(amax / 448) (1.0 when zero), codes = encode(fl(x / s)) -- the
+    fp8.py:132-151 recipe applied down the columns of each block.  Returns
+    (codes [M, C], scales [TB, C]) with TB = sum(ceil(M_g / 128)) rows, group by group.
+    """
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    rows, cols = x.shape
+    codes = np.empty((rows, cols), dtype=np.uint8)
+    blocks = []
+    off = 0
+    for m in group_sizes:
+        m = int(m)
+        for b0 in range(0, m, SCALE_BLOCK):
+            sl = slice(off + b0, off + min(b0 + SCALE_BLOCK, m))
+            amax = np.abs(x[sl]).max(axis=0)
+            s = np.where(amax > 0, amax / np.float32(E4M3_MAX), np.float32(1.0)).astype(np.float32)
+            blocks.append(s)
+            codes[sl] = encode(x[sl] / s[None, :])
+        off += m
+    scales = np.stack(blocks) if blocks else np.zeros((0, cols), np.float32)
+    return codes, scales

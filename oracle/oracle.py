@@ -39,6 +39,10 @@ def lib():
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
         ]
+        L.tagg_oracle_wgrad.restype = ctypes.c_int
+        L.tagg_oracle_wgrad.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.c_int]
         L.tagg_oracle_bf16_from_f32.restype = ctypes.c_uint16
         L.tagg_oracle_bf16_from_f32.argtypes = [ctypes.c_float]
         L.tagg_oracle_decode.restype = ctypes.c_float
@@ -100,3 +104,24 @@ def grouped_gemm(a_codes, a_scales, b_codes, b_scales, group_sizes, *, b_layout=
 
 def host_threads() -> int:
     return len(os.sched_getaffinity(0))
+
+
+def wgrad(x_codes, x_scales, dy_codes, dy_scales, group_sizes, *, threads=None):
+    """dW bits [G, K, N] (uint16) of the weight gradient X_g^T dY_g (tagg_oracle_wgrad).
+
+    x_codes [M, K], dy_codes [M, N]; x_scales [TB, K], dy_scales [TB, N]: one row per
+    (group, 128-token block), blocks numbered group by group.
+    """
+    x_codes = np.ascontiguousarray(x_codes, dtype=np.uint8)
+    dy_codes = np.ascontiguousarray(dy_codes, dtype=np.uint8)
+    x_scales = np.ascontiguousarray(x_scales, dtype=np.float32)
+    dy_scales = np.ascontiguousarray(dy_scales, dtype=np.float32)
+    sizes = np.ascontiguousarray(np.asarray(group_sizes, dtype=np.int64))
+    G = len(sizes)
+    K, N = x_codes.shape[1], dy_codes.shape[1]
+    out = np.zeros((G, K, N), dtype=np.uint16)
+    rc = lib().tagg_oracle_wgrad(_ptr(x_codes), _ptr(x_scales), _ptr(dy_codes), _ptr(dy_scales), _ptr(sizes),
+                                 G, K, N, _ptr(out), threads or 1)
+    if rc != 0:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return out

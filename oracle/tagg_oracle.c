@@ -187,3 +187,86 @@ int64_t tagg_oracle_pad_rows(const int64_t* group_sizes, int G, int block_rows) 
     total += ((group_sizes[g] + block_rows - 1) / block_rows) * block_rows - group_sizes[g];
   return total;
 }
+
+/*
+ * Weight-gradient oracle (the reference has no backward,
+ * SPEC.md:361, so this is the forward's arithmetic applied along the ragged axis):
+ *   dW[g][k][n] = bf16( acc ),  acc over the group's 128-token blocks j ascending:
+ *     inner_j = ascending-token chain of rounded f32 adds of exact products
+ *               x[t][k] * dy[t][n], t in block j  (_sequential_block_inner, engine.py:151-158)
+ *     s       = fl(sx[tb][k] * sdy[tb][n])              (_accumulate_scaled, engine.py:161-164)
+ *     acc     = fl(acc + fl(inner_j * s))
+ * x [M_total, K], dy [M_total, N] row-major codes; sx [TB, K], sdy [TB, N] with one row per
+ * (group, 128-token block), blocks numbered group by group (tb0(g) = sum of
+ * ceil(M_h/128) over h < g).  An empty group gives dW[g] = 0.  out: [G, K, N] bf16 bits.
+ */
+typedef struct {
+  const uint8_t *x, *dy;
+  const float *sx, *sdy;
+  const int64_t* group_sizes;
+  int G, K, N;
+  uint16_t* out;
+  int64_t job_begin, job_end; /* (g, k) pairs */
+} wjob_t;
+
+static void* wgrad_worker(void* arg) {
+  const wjob_t* j = (const wjob_t*)arg;
+  const int K = j->K, N = j->N;
+  float* inner = (float*)malloc((size_t)N * sizeof(float));
+  float* acc = (float*)malloc((size_t)N * sizeof(float));
+  for (int64_t p = j->job_begin; p < j->job_end; ++p) {
+    const int g = (int)(p / K), k = (int)(p % K);
+    int64_t off = 0, tb0 = 0;
+    for (int h = 0; h < g; ++h) {
+      off += j->group_sizes[h];
+      tb0 += (j->group_sizes[h] + 127) / 128;
+    }
+    const int64_t rows = j->group_sizes[g];
+    for (int n = 0; n < N; ++n) acc[n] = 0.0f;
+    for (int64_t b0 = 0; b0 < rows; b0 += 128) {
+      const int64_t b1 = (b0 + 128 < rows) ? b0 + 128 : rows;
+      for (int n = 0; n < N; ++n) inner[n] = 0.0f;
+      for (int64_t t = off + b0; t < off + b1; ++t) {
+        const float xv = g_decode[j->x[t * K + k]];
+        const uint8_t* dyr = j->dy + t * N;
+        for (int n = 0; n < N; ++n) inner[n] = inner[n] + xv * g_decode[dyr[n]];
+      }
+      const int64_t tb = tb0 + b0 / 128;
+      const float sxk = j->sx[tb * K + k];
+      const float* sdyr = j->sdy + tb * N;
+      for (int n = 0; n < N; ++n) {
+        const float s = sxk * sdyr[n];
+        const float t = inner[n] * s;
+        acc[n] = acc[n] + t;
+      }
+    }
+    uint16_t* o = j->out + ((int64_t)g * K + k) * N;
+    for (int n = 0; n < N; ++n) o[n] = tagg_oracle_bf16_from_f32(acc[n]);
+  }
+  free(inner);
+  free(acc);
+  return NULL;
+}
+
+int tagg_oracle_wgrad(const uint8_t* x, const float* sx, const uint8_t* dy, const float* sdy,
+                      const int64_t* group_sizes, int G, int K, int N, uint16_t* out, int nthreads) {
+  if (!g_decode_ready) build_decode_table();
+  if (G < 1 || K < 1 || N < 1) return -1;
+  for (int g = 0; g < G; ++g)
+    if (group_sizes[g] < 0) return -1;
+  const int64_t jobs_total = (int64_t)G * K;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if ((int64_t)nthreads > jobs_total) nthreads = (int)jobs_total;
+  wjob_t jobs[256];
+  pthread_t tids[256];
+  for (int t = 0; t < nthreads; ++t) {
+    wjob_t w = {x, dy, sx, sdy, group_sizes, G, K, N, out, jobs_total * t / nthreads,
+                jobs_total * (t + 1) / nthreads};
+    jobs[t] = w;
+  }
+  for (int t = 1; t < nthreads; ++t) pthread_create(&tids[t], NULL, wgrad_worker, &jobs[t]);
+  wgrad_worker(&jobs[0]);
+  for (int t = 1; t < nthreads; ++t) pthread_join(tids[t], NULL);
+  return 0;
+}

@@ -44,6 +44,7 @@ from .quant import (  # noqa: F401
     quantize_row_tiles,
     route_plan,
 )
+from .wgrad import quantize_col_blocks, wgrad_fp8  # noqa: F401
 from .planning import (  # noqa: F401
     account,
     build_pool,

@@ -30,6 +30,10 @@ SIGNATURES = {
     "tagg_unpad_rows": (c_int, [c_vp, c_vp, c_int, c_int, c_vp, c_i64, c_vp]),
     "tagg_padded_rows_bound": (c_i64, [c_i64, c_int]),
     "tagg_route_workspace_ints": (c_i64, [c_i64, c_int]),
+    "tagg_token_blocks_bound": (c_i64, [c_i64, c_int]),
+    "tagg_quantize_col_blocks": (c_int, [c_vp, c_int, c_i64, c_int, c_i64, c_vp, c_int, c_vp, c_i64, c_vp, c_vp,
+                                         c_vp]),
+    "tagg_wgrad_fp8": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_int, c_int, c_int, c_vp, c_vp]),
     "tagg_quantize_blocks": (c_int, [c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp,
                                      c_vp]),
     "tagg_route_plan": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp]),

@@ -44,6 +44,7 @@
 #include <mutex>
 
 #include "tagg.h"
+#include "tagg_host.h"
 #include "tagg_ptx.cuh"
 
 namespace tagg {
@@ -817,6 +818,12 @@ int gcd_int(int a, int b) {
 }
 
 }  // namespace
+
+bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const void* base, const uint64_t* dims,
+                const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw) {
+  return encode(m, dt, rank, base, dims, strides_bytes, box, sw);
+}
+int sm_count() { return num_sms_for_current_device(); }
 
 // Smem layout for a given stage count; returns total bytes (incl. alignment slack).
 static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_acc, uint32_t stage_bytes_b,

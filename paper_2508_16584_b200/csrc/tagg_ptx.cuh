@@ -382,6 +382,12 @@ __host__ __device__ constexpr uint32_t idesc_e4m3_f32(uint32_t m, uint32_t n, bo
          | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
+// Both operand majors selectable (the weight gradient reads A = X^T MN-major).
+__host__ __device__ constexpr uint32_t idesc_e4m3_f32_ab(uint32_t m, uint32_t n, bool a_mn_major, bool b_mn_major) {
+  return (1u << 4) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) | ((n >> 3) << 17) |
+         ((m >> 4) << 24);
+}
+
 // ---------------------------------------------------------------- promotion math
 // acc = fl(acc + p*s) on a pair of f32 (one FFMA2; a single rounding).
 __device__ __forceinline__ void ffma2(float& c0, float& c1, float p0, float p1, float s) {

@@ -1,0 +1,461 @@
+// tagg_wgrad.cu -- the MoE weight gradient as a K-grouped FP8 GEMM:
+//   dW_g = X_g^T dY_g,  X [M, K] and dY [M, N] in the padding-free grouped layout,
+// so the ragged per-expert row count M_g is the REDUCTION axis.  Operands carry one
+// fp32 scale per (group, 128-token block, column) -- quantize_col_blocks below -- and
+// the k-block promotion is the forward's (engine.py:151-164) with a per-element scale
+// s = fl(sx[tb][k] * sdy[tb][n]).  dW is bf16 [G, K, N].
+//
+// The paper's mechanism moves to the loads: a group's last token block has res < 128
+// rows, and the rows after it belong to the next expert.  The producer loads it with
+// the power-of-two descriptor pool (heights 1..128) in two phases, rows [0, d) and
+// [res-d, res) with d = 2^floor(log2 res) (descriptors.py:95-106 applied to loads), and
+// zeroes smem rows [res, 128) so the MMA's reduction sees exact zeros: no row of
+// another group is ever read into the product, and nothing is padded in HBM.
+//
+// Persistent 1-CTA tiles of 128 (K) x 128 (N), tcgen05.mma cta_group::1 M=128 N=128,
+// A = X^T and B = dY both MN-major in 128B-swizzled smem (token rows), 4 TMEM
+// accumulation buffers, warp roles as in tagg_gemm.cu (producer, MMA, 8 promotion warps).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "tagg.h"
+#include "tagg_host.h"
+#include "tagg_ptx.cuh"
+
+namespace tagg {
+namespace wg {
+
+constexpr int BT = 128;                 // tokens per k-block
+constexpr int kThreads = 384;
+constexpr int kPromoWarps = 8;
+constexpr int kNumAcc = 4;              // TMEM buffers of 128 columns
+constexpr int kStages = 4;
+constexpr int kScaleRing = 8;           // k-block scale slots (sx 128 + sdy 128 floats)
+constexpr uint32_t kStageA = BT * 128;  // 128 token rows x 128 K columns
+constexpr uint32_t kStageB = BT * 128;  // 128 token rows x 128 N columns
+constexpr uint32_t kScaleSlot = 2 * 128 * 4;
+constexpr uint32_t kChunkC = 128 * 128;  // 128 rows x 64 bf16 columns
+constexpr int kPool = 8;
+
+struct Params {
+  CUtensorMap map_x[kPool];   // X [M, K] u8, box {128 cols, 2^i rows}, SW128
+  CUtensorMap map_dy[kPool];  // dY [M, N] u8, box {128 cols, 2^i rows}, SW128
+  CUtensorMap map_dw;         // dW [G*K, N] bf16, box {64 cols, 128 rows}, SW128
+  const float* sx;            // [TB, K]
+  const float* sdy;           // [TB, N]
+  const int32_t* group_sizes;
+  int G, K, N, KT, NT;
+  uint32_t off_a, off_b, off_c, off_s, off_tab, off_bar;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constant__ Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = p.G;
+  int32_t* tab_off = reinterpret_cast<int32_t*>(smem + p.off_tab);  // [G] first row
+  int32_t* tab_tb = tab_off + G;                                      // [G] first token block
+  int32_t* tab_m = tab_tb + G;                                        // [G] rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + kNumAcc;
+  uint64_t* sfull = tempty + kNumAcc;
+  uint64_t* sempty = sfull + kScaleRing;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + kScaleRing);
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < kNumAcc; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kPromoWarps);
+    }
+    for (int i = 0; i < kScaleRing; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sempty[i], kPromoWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
+  if (warp == 2) {
+    int carry_r = 0, carry_b = 0;
+    for (int base = 0; base < G; base += 32) {
+      const int g = base + lane;
+      const int m = (g < G) ? max(0, p.group_sizes[g]) : 0;
+      const int nb = (m + BT - 1) / BT;
+      int im = m, ib = nb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, im, o);
+        const int y = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) { im += x; ib += y; }
+      }
+      if (g < G) {
+        tab_off[g] = carry_r + im - m;
+        tab_tb[g] = carry_b + ib - nb;
+        tab_m[g] = m;
+      }
+      carry_r += __shfl_sync(0xffffffffu, im, 31);
+      carry_b += __shfl_sync(0xffffffffu, ib, 31);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const int tiles = G * p.KT * p.NT;
+
+  if (warp < 4) {
+    setmaxnreg_dec<72>();
+    if (warp == 0) {
+      // ====================================================== producer
+      uint32_t stage = 0, phase = 0, sring = 0, sph = 0;
+      const uint32_t sA0 = smem_u32(smem + p.off_a), sB0 = smem_u32(smem + p.off_b);
+      const uint32_t sS0 = smem_u32(smem + p.off_s);
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
+        const int k0 = (rem / p.NT) * 128, n0 = (rem % p.NT) * 128;
+        const int m = tab_m[g], off = tab_off[g], tb0 = tab_tb[g];
+        for (int j = 0; j * BT < m; ++j) {
+          // scales of this token block: sx[tb][k0..+128), sdy[tb][n0..+128)
+          mbar_wait_addr(smem_u32(&sempty[sring]), sph ^ 1);
+          if (lane == 0) {
+            const uint32_t dst = sS0 + sring * kScaleSlot;
+            const int64_t tb = tb0 + j;
+            mbar_arrive_expect_tx_addr(smem_u32(&sfull[sring]), kScaleSlot);
+            bulk_load_1d_addr(dst, p.sx + tb * p.K + k0, 512, smem_u32(&sfull[sring]));
+            bulk_load_1d_addr(dst + 512, p.sdy + tb * p.N + n0, 512, smem_u32(&sfull[sring]));
+          }
+          if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
+          // operands
+          mbar_wait_addr(smem_u32(&empty[stage]), phase ^ 1);
+          const int res = min(BT, m - j * BT);
+          const int row0 = off + j * BT;
+          const uint32_t a_dst = sA0 + stage * kStageA, b_dst = sB0 + stage * kStageB;
+          if (res < BT) {
+            // zero the rows past the group end (the next expert's tokens are never read)
+            const int zrows = BT - res;
+            for (int i = lane; i < zrows * 8; i += 32) {
+              const uint32_t off16 = static_cast<uint32_t>((res + i / 8) * 128 + (i % 8) * 16);
+              st_shared_v4(a_dst + off16, 0u, 0u, 0u, 0u);
+              st_shared_v4(b_dst + off16, 0u, 0u, 0u, 0u);
+            }
+            fence_proxy_async_smem();
+          }
+          __syncwarp();
+          if (lane == 0) {
+            const uint32_t fb = smem_u32(&full[stage]);
+            if (res == BT) {
+              mbar_arrive_expect_tx_addr(fb, kStageA + kStageB);
+              tma_load_2d_u32<1>(&p.map_x[7], fb, a_dst, k0, row0);
+              tma_load_2d_u32<1>(&p.map_dy[7], fb, b_dst, n0, row0);
+            } else {
+              // dual-phase load from the pool: rows [0, d) and [res - d, res)
+              const int lg = 31 - __clz(res), d = 1 << lg;
+              mbar_arrive_expect_tx_addr(fb, 4u * d * 128u);
+              tma_load_2d_u32<1>(&p.map_x[lg], fb, a_dst, k0, row0);
+              tma_load_2d_u32<1>(&p.map_x[lg], fb, a_dst + (res - d) * 128u, k0, row0 + res - d);
+              tma_load_2d_u32<1>(&p.map_dy[lg], fb, b_dst, n0, row0);
+              tma_load_2d_u32<1>(&p.map_dy[lg], fb, b_dst + (res - d) * 128u, n0, row0 + res - d);
+            }
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+      if (lane == 0)
+        for (int i = 0; i < kStages; ++i) {
+          mbar_wait_addr(smem_u32(&empty[stage]), phase ^ 1);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      __syncwarp();
+    } else if (warp == 1) {
+      // ====================================================== MMA (whole warp, elected issue)
+      const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
+      const uint32_t idesc = idesc_e4m3_f32_ab(128, 128, true, true);
+      // MN-major operands: 128 token rows of 128 B (one swizzle atom wide), 8-row groups
+      // of 1 KB; K = 32 tokens per MMA = 32 rows = 4 KB
+      const uint64_t a0 = umma_desc_sw128(smem_u32(smem + p.off_a), kStageA, 1024);
+      const uint64_t b0 = umma_desc_sw128(smem_u32(smem + p.off_b), kStageB, 1024);
+      uint32_t stage = 0, phase = 0, acc = 0, accph = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int g = t / (p.KT * p.NT);
+        const int m = tab_m[g];
+        for (int j = 0; j * BT < m; ++j) {
+          mbar_wait_addr(smem_u32(&tempty[acc]), accph ^ 1);
+          mbar_wait_addr(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const uint64_t ad = a0 + ((stage * kStageA) >> 4), bd = b0 + ((stage * kStageB) >> 4);
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_f8f6f4<1>(tmem_base + acc * 128, ad + static_cast<uint64_t>(k * 256),
+                            bd + static_cast<uint64_t>(k * 256), idesc, k > 0 ? 1u : 0u);
+            mma_commit_addr<1>(smem_u32(&empty[stage]));
+            mma_commit_addr<1>(smem_u32(&tfull[acc]));
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++acc == kNumAcc) { acc = 0; accph ^= 1; }
+        }
+      }
+    }
+  } else {
+    setmaxnreg_inc<216>();
+    // ====================================================== promotion + epilogue
+    const uint32_t tmem_base = opaque_u32(ld_shared_u32(smem_u32(tmem_slot)));
+    const int pw = warp - 4, q = warp & 3, half = pw >> 2;
+    const int r = 32 * q + lane;  // dW row within the tile (K index k0 + r)
+    const int ptid = threadIdx.x - 128;
+    const uint32_t t_lane = static_cast<uint32_t>(32 * q) << 16;
+    const uint32_t sS0 = opaque_u32(smem_u32(smem + p.off_s));
+    const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
+    const uint32_t sfull0 = opaque_u32(smem_u32(&sfull[0])), sempty0 = opaque_u32(smem_u32(&sempty[0]));
+    uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
+      const int k0 = (rem / p.NT) * 128, n0 = (rem % p.NT) * 128;
+      const int m = tab_m[g];
+      float acc[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
+      for (int j = 0; j * BT < m; ++j) {
+        mbar_wait_addr(sfull0 + 8 * sring, sph);
+        const uint32_t slot = sS0 + sring * kScaleSlot;
+        const float sxk = ld_shared_f32(slot + 4u * r);
+        const uint32_t sdy = slot + 512u + 4u * (64u * half);
+        mbar_wait_addr(tfull0 + 8 * acc_i, accph);
+        tc_fence_after();
+        uint32_t v[64];
+        tmem_ld_32x32b_x64(tmem_base + t_lane + acc_i * 128 + 64u * half, v);
+        tmem_wait_ld_dep64(v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_addr(tempty0 + 8 * acc_i);
+#pragma unroll
+        for (int c = 0; c < 64; c += 4) {
+          float4 sd;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(sd.x), "=f"(sd.y), "=f"(sd.z), "=f"(sd.w)
+                       : "r"(sdy + 4u * c));
+          // s = fl(sx * sdy); acc = fl(acc + fl(inner * s)) with the product rounding
+          // folded into one FMA (as the forward's default promotion)
+          acc[c + 0] = __fmaf_rn(__uint_as_float(v[c + 0]), __fmul_rn(sxk, sd.x), acc[c + 0]);
+          acc[c + 1] = __fmaf_rn(__uint_as_float(v[c + 1]), __fmul_rn(sxk, sd.y), acc[c + 1]);
+          acc[c + 2] = __fmaf_rn(__uint_as_float(v[c + 2]), __fmul_rn(sxk, sd.z), acc[c + 2]);
+          acc[c + 3] = __fmaf_rn(__uint_as_float(v[c + 3]), __fmul_rn(sxk, sd.w), acc[c + 3]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_addr(sempty0 + 8 * sring);
+        if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
+        if (++acc_i == kNumAcc) { acc_i = 0; accph ^= 1; }
+      }
+      // epilogue: bf16 -> 128B-swizzled staging, warp half h -> chunk h (64 columns)
+      if (ptid == 0) bulk_wait_read0();
+      named_bar_sync(1, 32 * kPromoWarps);
+      {
+        const uint32_t base = smem_u32(smem + p.off_c) + half * kChunkC + static_cast<uint32_t>(r) * 128u;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const uint32_t w0 = pack_bf16x2(acc[8 * jj + 0], acc[8 * jj + 1]);
+          const uint32_t w1 = pack_bf16x2(acc[8 * jj + 2], acc[8 * jj + 3]);
+          const uint32_t w2 = pack_bf16x2(acc[8 * jj + 4], acc[8 * jj + 5]);
+          const uint32_t w3 = pack_bf16x2(acc[8 * jj + 6], acc[8 * jj + 7]);
+          st_shared_v4(base + static_cast<uint32_t>((jj ^ (r & 7)) * 16), w0, w1, w2, w3);
+        }
+        fence_proxy_async_smem();
+      }
+      named_bar_sync(1, 32 * kPromoWarps);
+      if (ptid == 0) {
+        const int row = g * p.K + k0;
+        tma_store_2d(&p.map_dw, smem + p.off_c, n0, row);
+        tma_store_2d(&p.map_dw, smem + p.off_c + kChunkC, n0 + 64, row);
+        bulk_commit();
+      }
+    }
+    if (ptid == 0) bulk_wait0();
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<1>(ld_shared_u32(smem_u32(tmem_slot)), 512);
+  }
+}
+
+// Per-group 128x1 column-block quantizer: CTA (row block y, column chunk x), thread =
+// one column; pass 1 takes the block's amax, pass 2 (L2-resident re-read) quantizes.
+template <bool kBf16>
+__global__ void __launch_bounds__(128) quantize_col_blocks_kernel(const void* __restrict__ x, int64_t ldx, int cols,
+                                                                  const int32_t* __restrict__ group_sizes, int G,
+                                                                  uint8_t* __restrict__ codes, int64_t ldc,
+                                                                  float* __restrict__ scales, int32_t* err) {
+  __shared__ int32_t s_row0, s_rows, s_tb;
+  if (threadIdx.x < 32) {
+    // which (group, block) is this CTA's: walk the group table
+    const int lane = threadIdx.x;
+    int carry_r = 0, carry_b = 0, found = 0;
+    const int want = blockIdx.y;
+    for (int base = 0; base < G && !found; base += 32) {
+      const int g = base + lane;
+      const int m = (g < G) ? max(0, group_sizes[g]) : 0;
+      const int nb = (m + 127) / 128;
+      int im = m, ib = nb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, im, o);
+        const int b = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) { im += a; ib += b; }
+      }
+      const int b0 = carry_b + ib - nb, r0 = carry_r + im - m;
+      const bool mine = g < G && want >= b0 && want < b0 + nb;
+      const uint32_t hit = __ballot_sync(0xffffffffu, mine);
+      if (hit) {
+        found = 1;
+        if (mine) {
+          const int j = want - b0;
+          s_row0 = r0 + 128 * j;
+          s_rows = min(128, m - 128 * j);
+          s_tb = want;
+        }
+      }
+      carry_r += __shfl_sync(0xffffffffu, im, 31);
+      carry_b += __shfl_sync(0xffffffffu, ib, 31);
+    }
+    if (!found && lane == 0) s_rows = 0;
+  }
+  __syncthreads();
+  const int rows = s_rows;
+  if (rows <= 0) return;
+  const int64_t row0 = s_row0;
+  const int c = blockIdx.x * 128 + threadIdx.x;
+  if (c >= cols) return;
+  auto ld = [&](int64_t rr) -> float {
+    if constexpr (kBf16)
+      return __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(x)[rr * ldx + c]) << 16);
+    else
+      return reinterpret_cast<const float*>(x)[rr * ldx + c];
+  };
+  float amax = 0.0f;
+  bool bad = false;
+  for (int i = 0; i < rows; ++i) {
+    const float m = fabsf(ld(row0 + i));
+    bad |= !(m <= 3.402823466e38f);
+    amax = fmaxf(amax, m);
+  }
+  const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  scales[static_cast<int64_t>(s_tb) * cols + c] = s;
+  for (int i = 0; i < rows; i += 2) {
+    const float v0 = __fdiv_rn(ld(row0 + i), s);
+    const float v1 = (i + 1 < rows) ? __fdiv_rn(ld(row0 + i + 1), s) : 0.0f;
+    uint16_t pair;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(pair) : "f"(v1), "f"(v0));
+    codes[(row0 + i) * ldc + c] = static_cast<uint8_t>(pair & 0xFF);
+    if (i + 1 < rows) codes[(row0 + i + 1) * ldc + c] = static_cast<uint8_t>(pair >> 8);
+  }
+  if (bad) atomicOr(err, 2);
+}
+
+}  // namespace wg
+}  // namespace tagg
+
+using namespace tagg;
+
+extern "C" int64_t tagg_token_blocks_bound(int64_t m_alloc, int G) {
+  if (m_alloc < 0 || G < 1) return 0;
+  return (m_alloc + 127) / 128 + G;
+}
+
+extern "C" int tagg_quantize_col_blocks(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
+                                        const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
+                                        int32_t* err_flag, void* stream) {
+  if (x_dtype != TAGG_DTYPE_BF16 && x_dtype != TAGG_DTYPE_F32) return TAGG_ERR_CONFIG;
+  if (G < 1 || cols < 1 || m_alloc < 0 || ldx < cols || ldc < cols) return TAGG_ERR_SHAPE;
+  if (m_alloc == 0) return TAGG_OK;
+  if (!x || !group_sizes || !codes || !scales || !err_flag) return TAGG_ERR_SHAPE;
+  const int64_t tb = tagg_token_blocks_bound(m_alloc, G);
+  if (tb > 65535) return TAGG_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 grid(static_cast<unsigned>((cols + 127) / 128), static_cast<unsigned>(tb));
+  if (x_dtype == TAGG_DTYPE_BF16)
+    wg::quantize_col_blocks_kernel<true><<<grid, 128, 0, st>>>(x, ldx, cols, group_sizes, G,
+                                                               static_cast<uint8_t*>(codes), ldc, scales, err_flag);
+  else
+    wg::quantize_col_blocks_kernel<false><<<grid, 128, 0, st>>>(x, ldx, cols, group_sizes, G,
+                                                                static_cast<uint8_t*>(codes), ldc, scales, err_flag);
+  return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
+}
+
+extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, const float* sdy, int64_t m_alloc,
+                              const int32_t* group_sizes, int G, int K, int N, void* dw, void* stream) {
+  using namespace tagg::wg;
+  if (G < 1 || K < 128 || N < 128 || K % 128 || N % 128) return TAGG_ERR_CONFIG;
+  if (m_alloc < 0) return TAGG_ERR_SHAPE;
+  if (!x || !sx || !dy || !sdy || !group_sizes || !dw) return TAGG_ERR_SHAPE;
+  auto mis = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) != 0; };
+  if (mis(x) || mis(dy) || mis(dw) || mis(sx) || mis(sdy)) return TAGG_ERR_ALIGNMENT;
+  if (static_cast<int64_t>(G) * K >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
+  const int sms = sm_count();
+  if (sms <= 0) return TAGG_ERR_CUDA;
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  const int64_t rows = std::max<int64_t>(m_alloc, 1);
+  for (int i = 0; i < kPool; ++i) {
+    const uint32_t box[2] = {128, 1u << i};
+    const uint64_t dx[2] = {static_cast<uint64_t>(K), static_cast<uint64_t>(rows)};
+    const uint64_t sxs[1] = {static_cast<uint64_t>(K)};
+    const uint64_t dd[2] = {static_cast<uint64_t>(N), static_cast<uint64_t>(rows)};
+    const uint64_t sds[1] = {static_cast<uint64_t>(N)};
+    if (!encode_map(&p.map_x[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, x, dx, sxs, box, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_map(&p.map_dy[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dy, dd, sds, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return TAGG_ERR_CUDA;
+  }
+  {
+    const uint32_t box[2] = {64, 128};
+    const uint64_t d[2] = {static_cast<uint64_t>(N), static_cast<uint64_t>(G) * K};
+    const uint64_t s[1] = {static_cast<uint64_t>(N) * 2};
+    if (!encode_map(&p.map_dw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dw, d, s, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return TAGG_ERR_CUDA;
+  }
+  p.sx = sx;
+  p.sdy = sdy;
+  p.group_sizes = group_sizes;
+  p.G = G;
+  p.K = K;
+  p.N = N;
+  p.KT = K / 128;
+  p.NT = N / 128;
+  p.off_a = 0;
+  p.off_b = p.off_a + kStages * kStageA;
+  p.off_c = p.off_b + kStages * kStageB;
+  p.off_s = p.off_c + 2 * kChunkC;
+  p.off_tab = p.off_s + kScaleRing * kScaleSlot;
+  const uint32_t tab = static_cast<uint32_t>(((3 * G * 4) + 15) & ~15);
+  p.off_bar = p.off_tab + tab;
+  const uint32_t smem = p.off_bar + (2 * kStages + 2 * kNumAcc + 2 * kScaleRing) * 8 + 16 + 1024;
+  if (smem > 232448) return TAGG_ERR_UNSUPPORTED;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448) != cudaSuccess)
+      return TAGG_ERR_CUDA;
+    configured = true;
+  }
+  const int64_t tiles = static_cast<int64_t>(G) * p.KT * p.NT;
+  const int grid = static_cast<int>(std::min<int64_t>(sms, tiles));
+  wgrad_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    std::fprintf(stderr, "tagg_wgrad_fp8: launch failed: %s\n", cudaGetErrorString(e));
+    return TAGG_ERR_CUDA;
+  }
+  return TAGG_OK;
+}

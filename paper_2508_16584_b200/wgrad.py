@@ -1,0 +1,71 @@
+"""Backward: the MoE weight gradient as a K-grouped FP8 GEMM.
+
+dW_g = X_g^T dY_g over each expert's ragged rows, from operands quantized per
+(group, 128-token block, column) -- the forward's 1x128 recipe (fp8.py:132-151) turned
+to run down the token axis, which is the reduction axis here.  Kernels:
+csrc/tagg_wgrad.cu through the C ABI.  dgrad needs no new kernel: it is the forward
+grouped GEMM with K-major B (grouped_gemm_fp8(..., b_layout="nk")).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from ._lib import lib
+from .errors import InvalidInput, ShapeMismatch, raise_for_status
+from .quant import _DTYPES, _check_cuda, _stream
+
+
+def quantize_col_blocks(x: torch.Tensor, group_sizes: torch.Tensor, *, check: bool = False):
+    """(codes uint8 [M, C], scales f32 [TB_bound, C]) for x [M, C] in the grouped layout.
+
+    Scale row tb holds the tb-th (group, 128-token block) in group order; only the first
+    sum(ceil(M_g/128)) rows are defined (group sizes stay on the device: no host sync).
+    """
+    _check_cuda(x, "x")
+    if x.dim() != 2:
+        raise InvalidInput("expected a 2-D matrix")
+    if x.dtype not in _DTYPES:
+        x = x.to(torch.float32)
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    if group_sizes.dtype != torch.int32 or not group_sizes.is_cuda:
+        raise ShapeMismatch("group_sizes must be an int32 CUDA tensor")
+    m, c = x.shape
+    g = group_sizes.numel()
+    tb = lib().tagg_token_blocks_bound(m, g)
+    codes = torch.empty((m, c), dtype=torch.uint8, device=x.device)
+    scales = torch.empty((max(tb, 1), c), dtype=torch.float32, device=x.device)
+    err = torch.zeros(1, dtype=torch.int32, device=x.device)
+    rc = lib().tagg_quantize_col_blocks(x.data_ptr(), _DTYPES[x.dtype], m, c, x.stride(0), group_sizes.data_ptr(),
+                                        g, codes.data_ptr(), c, scales.data_ptr(), err.data_ptr(), _stream())
+    raise_for_status(rc, "tagg_quantize_col_blocks")
+    if check and int(err.item()):
+        raise InvalidInput("matrix entries must be finite")
+    return codes, scales
+
+
+def wgrad_fp8(x_codes, x_scales, dy_codes, dy_scales, group_sizes, out=None) -> torch.Tensor:
+    """dW [G, K, N] bf16 = X_g^T dY_g per group (K, N multiples of 128)."""
+    for t, what in ((x_codes, "x_codes"), (dy_codes, "dy_codes")):
+        _check_cuda(t, what)
+    if x_codes.dtype == torch.float8_e4m3fn:
+        x_codes = x_codes.view(torch.uint8)
+    if dy_codes.dtype == torch.float8_e4m3fn:
+        dy_codes = dy_codes.view(torch.uint8)
+    m, k = x_codes.shape
+    n = dy_codes.shape[1]
+    if dy_codes.shape[0] != m:
+        raise ShapeMismatch("X and dY need the same rows")
+    for t in (x_codes, dy_codes, x_scales, dy_scales):
+        if not t.is_contiguous():
+            raise ShapeMismatch("operands must be contiguous")
+    if x_scales.shape[1] != k or dy_scales.shape[1] != n:
+        raise ShapeMismatch("scales must be [TB, K] and [TB, N]")
+    g = group_sizes.numel()
+    if out is None:
+        out = torch.empty((g, k, n), dtype=torch.bfloat16, device=x_codes.device)
+    rc = lib().tagg_wgrad_fp8(x_codes.data_ptr(), x_scales.data_ptr(), dy_codes.data_ptr(), dy_scales.data_ptr(), m,
+                              group_sizes.data_ptr(), g, k, n, out.data_ptr(), _stream())
+    raise_for_status(rc, "tagg_wgrad_fp8")
+    return out

@@ -1,0 +1,83 @@
+"""Weight gradient as a K-grouped FP8 GEMM (csrc/tagg_wgrad.cu) against the oracle.
+
+The ragged per-expert row count is the reduction axis: every residue M_g mod 128
+(dual-phase pool loads + zeroed tail rows), empty groups, and the per-(group, token
+block, column) quantizer (bit-exact vs oracle/fp8.quantize_col_blocks).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2508_16584_b200 as tg
+from helpers import assert_parity
+from oracle import fp8 as ofp8
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0)
+
+
+def _data(sizes, k, n, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    m = sum(sizes)
+    x = rng.standard_normal((m, k)).astype(np.float32) * np.exp2(rng.integers(-3, 4, size=(m, 1))).astype(np.float32)
+    dy = rng.standard_normal((m, n)).astype(np.float32) * np.exp2(rng.integers(-3, 4, size=(m, 1))).astype(np.float32)
+    return x, dy
+
+
+@pytest.mark.parametrize("sizes", [(200,), (1, 0, 129, 255, 384), tuple(128 * (g % 3) + (g * 37) % 128 + 1 for g in range(8))])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_quantize_col_blocks_is_bit_exact(sizes, dtype):
+    x, _ = _data(sizes, 384, 128, 1)
+    xt = torch.from_numpy(x).to(DEV).to(dtype)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    codes, scales = tg.quantize_col_blocks(xt, gs, check=True)
+    torch.cuda.synchronize()
+    want_c, want_s = ofp8.quantize_col_blocks(xt.float().cpu().numpy(), sizes)
+    np.testing.assert_array_equal(codes.cpu().numpy(), want_c)
+    tb = want_s.shape[0]
+    np.testing.assert_array_equal(scales[:tb].cpu().numpy().view(np.uint32), want_s.view(np.uint32))
+
+
+@pytest.mark.parametrize("sizes,k,n", [
+    ((128,), 128, 128),
+    ((300, 0, 1, 77, 256), 256, 384),
+    (tuple(range(1, 128, 9)), 128, 256),       # every residue class, ragged reduction
+    ((1000, 513), 384, 256),
+])
+def test_wgrad_matches_oracle(sizes, k, n):
+    x, dy = _data(sizes, k, n, sum(sizes))
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    xc, xs = tg.quantize_col_blocks(torch.from_numpy(x).to(DEV), gs)
+    dc, ds = tg.quantize_col_blocks(torch.from_numpy(dy).to(DEV), gs)
+    dw = tg.wgrad_fp8(xc, xs, dc, ds, gs)
+    torch.cuda.synchronize()
+    tb = sum(-(-s // 128) for s in sizes)
+    want = orc.wgrad(xc.cpu().numpy(), xs[:tb].cpu().numpy(), dc.cpu().numpy(), ds[:tb].cpu().numpy(), sizes,
+                     threads=8)
+    got = dw.view(torch.int16).cpu().numpy().view(np.uint16)
+    for g, m in enumerate(sizes):
+        if m == 0:
+            assert np.all(got[g] == 0), "an empty group's gradient is zero"
+        else:
+            assert_parity(got[g], want[g], label=f"group {g} (M_g={m})")
+
+
+def test_wgrad_never_reads_the_next_group():
+    """Poison the rows after a short group: its gradient must not change."""
+    sizes = (70, 300)
+    k, n = 128, 128
+    x, dy = _data(sizes, k, n, 5)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    xc, xs = tg.quantize_col_blocks(torch.from_numpy(x).to(DEV), gs)
+    dc, ds = tg.quantize_col_blocks(torch.from_numpy(dy).to(DEV), gs)
+    base = tg.wgrad_fp8(xc, xs, dc, ds, gs)[0].clone()
+    xc2, dc2 = xc.clone(), dc.clone()
+    xc2[70:198] = 0x7E  # large codes in the rows a full 128-row box would have read
+    dc2[70:198] = 0x7E
+    again = tg.wgrad_fp8(xc2, xs, dc2, ds, gs)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(base.view(torch.int16), again.view(torch.int16))
