@@ -512,7 +512,35 @@ def run_extra(torch, tg, dev, rank, fp8_peak, exact):
         del P
         torch.cuda.empty_cache()
     out["quantize_dispatch_dsv3"] = run_quantize_dispatch(torch, tg, dev)
+    out["wgrad_dsv3_gateup"] = run_wgrad(torch, tg, dev, fp8_peak)
     return out
+
+
+def run_wgrad(torch, tg, dev, fp8_peak, iters=5, warmup=2):
+    """dW_g = X_g^T dY_g for the DeepSeek-V3 gate+up shapes (32 local
+    experts, skewed M_g, K=7168, N=4096): the ragged rows are the reduction axis."""
+    _, sizes = deepseek_gateup_sizes(seed=0)
+    sizes = [int(s) for s in sizes]
+    m, k, n = sum(sizes), 7168, 4096
+    gen = torch.Generator(device=dev).manual_seed(5)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=dev)
+    xc, xs = tg.quantize_col_blocks(torch.randn((m, k), device=dev, generator=gen).to(torch.bfloat16), gs)
+    dc, ds = tg.quantize_col_blocks(torch.randn((m, n), device=dev, generator=gen).to(torch.bfloat16), gs)
+    dw = torch.empty((len(sizes), k, n), dtype=torch.bfloat16, device=dev)
+    for _ in range(warmup):
+        tg.wgrad_fp8(xc, xs, dc, ds, gs, out=dw)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        tg.wgrad_fp8(xc, xs, dc, ds, gs, out=dw)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / iters
+    flops = 2.0 * m * k * n
+    return {"groups": len(sizes), "rows": m, "K": k, "N": n, "ms": ms, "tflops": flops / ms / 1e9,
+            "fp8_peak_frac": flops / ms / 1e9 / fp8_peak, "dw_bytes": len(sizes) * k * n * 2,
+            "tile": "1-CTA 128x128, cta_group::1"}
 
 
 def run_quantize_dispatch(torch, tg, dev, tokens=32768, k=7168, topk=8, experts=256, iters=10, warmup=3):

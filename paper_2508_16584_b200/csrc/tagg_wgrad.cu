@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     const uint32_t sS0 = opaque_u32(smem_u32(smem + p.off_s));
     const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
     const uint32_t sfull0 = opaque_u32(smem_u32(&sfull[0])), sempty0 = opaque_u32(smem_u32(&sempty[0]));
-    uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0;
+    uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0, tiles_done = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
       const int k0 = (rem / p.NT) * 128, n0 = (rem % p.NT) * 128;
@@ -258,11 +258,13 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
         if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
         if (++acc_i == kNumAcc) { acc_i = 0; accph ^= 1; }
       }
-      // epilogue: bf16 -> 128B-swizzled staging, warp half h -> chunk h (64 columns)
-      if (ptid == 0) bulk_wait_read0();
+      // epilogue: bf16 -> 128B-swizzled staging (double-buffered across tiles, so the
+      // previous tile's stores drain while this one is written), warp half h -> chunk h
+      const uint32_t sbuf = (tiles_done & 1) * 2 * kChunkC;
+      if (ptid == 0) bulk_wait_read1();
       named_bar_sync(1, 32 * kPromoWarps);
       {
-        const uint32_t base = smem_u32(smem + p.off_c) + half * kChunkC + static_cast<uint32_t>(r) * 128u;
+        const uint32_t base = smem_u32(smem + p.off_c) + sbuf + half * kChunkC + static_cast<uint32_t>(r) * 128u;
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
           const uint32_t w0 = pack_bf16x2(acc[8 * jj + 0], acc[8 * jj + 1]);
@@ -276,10 +278,11 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
       named_bar_sync(1, 32 * kPromoWarps);
       if (ptid == 0) {
         const int row = g * p.K + k0;
-        tma_store_2d(&p.map_dw, smem + p.off_c, n0, row);
-        tma_store_2d(&p.map_dw, smem + p.off_c + kChunkC, n0 + 64, row);
+        tma_store_2d(&p.map_dw, smem + p.off_c + sbuf, n0, row);
+        tma_store_2d(&p.map_dw, smem + p.off_c + sbuf + kChunkC, n0 + 64, row);
         bulk_commit();
       }
+      ++tiles_done;
     }
     if (ptid == 0) bulk_wait0();
   }
@@ -437,7 +440,7 @@ extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, co
   p.off_a = 0;
   p.off_b = p.off_a + kStages * kStageA;
   p.off_c = p.off_b + kStages * kStageB;
-  p.off_s = p.off_c + 2 * kChunkC;
+  p.off_s = p.off_c + 4 * kChunkC;  // two staging buffers of 2 chunks
   p.off_tab = p.off_s + kScaleRing * kScaleSlot;
   const uint32_t tab = static_cast<uint32_t>(((3 * G * 4) + 15) & ~15);
   p.off_bar = p.off_tab + tab;
