@@ -59,3 +59,17 @@ def _(x, expert_ids, num_experts):
     rows = expert_ids.numel()
     return (x.new_empty((rows, k), dtype=torch.uint8), x.new_empty((rows, -(-k // 128)), dtype=torch.float32),
             x.new_empty((num_experts,), dtype=torch.int32), x.new_empty((rows,), dtype=torch.int32))
+
+
+@torch.library.custom_op(f"{_LIB}::wgrad_fp8", mutates_args=(), device_types="cuda")
+def wgrad_fp8(x_codes: torch.Tensor, x_scales: torch.Tensor, dy_codes: torch.Tensor, dy_scales: torch.Tensor,
+              group_sizes: torch.Tensor) -> torch.Tensor:
+    """dW [G, K, N] bf16 = X_g^T dY_g (the K-grouped weight gradient)."""
+    from . import wgrad
+
+    return wgrad.wgrad_fp8(x_codes, x_scales, dy_codes, dy_scales, group_sizes)
+
+
+@wgrad_fp8.register_fake
+def _(x_codes, x_scales, dy_codes, dy_scales, group_sizes):
+    return x_codes.new_empty((group_sizes.shape[0], x_codes.shape[1], dy_codes.shape[1]), dtype=torch.bfloat16)

@@ -11,7 +11,7 @@ import paper_2508_16584_b200 as tg  # noqa: F401  (registers the ops)
 
 
 def test_ops_are_registered():
-    for name in ("grouped_gemm_fp8", "quantize_row_tiles", "quantize_dispatch"):
+    for name in ("grouped_gemm_fp8", "quantize_row_tiles", "quantize_dispatch", "wgrad_fp8"):
         assert hasattr(torch.ops.tagg, name)
 
 
@@ -37,6 +37,8 @@ def test_fake_kernels_infer_shapes():
         e = torch.empty((10, 4), dtype=torch.int32, device="cuda")
         ac, asc, gsz, dest = torch.ops.tagg.quantize_dispatch(x, e, 16)
         assert ac.shape == (40, 300) and asc.shape == (40, 3) and gsz.shape == (16,) and dest.shape == (40,)
+        dw = torch.ops.tagg.wgrad_fp8(a[:, :256], sa, a[:, :128], sa, gs)
+        assert dw.shape == (3, 256, 128) and dw.dtype == torch.bfloat16
 
 
 @pytest.mark.gpu
