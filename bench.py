@@ -540,7 +540,7 @@ def run_wgrad(torch, tg, dev, fp8_peak, iters=5, warmup=2):
     flops = 2.0 * m * k * n
     return {"groups": len(sizes), "rows": m, "K": k, "N": n, "ms": ms, "tflops": flops / ms / 1e9,
             "fp8_peak_frac": flops / ms / 1e9 / fp8_peak, "dw_bytes": len(sizes) * k * n * 2,
-            "tile": "1-CTA 128x128, cta_group::1"}
+            "tile": "CTA pair 256x256, cta_group::2"}
 
 
 def run_quantize_dispatch(torch, tg, dev, tokens=32768, k=7168, topk=8, experts=256, iters=10, warmup=3):

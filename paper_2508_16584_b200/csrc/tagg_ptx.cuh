@@ -406,6 +406,32 @@ __device__ __forceinline__ void ffma2(float& c0, float& c1, float p0, float p1, 
       : "f"(p0), "f"(p1), "f"(s));
 }
 
+// (c0, c1) = fl((a0, a1) * (b0, b1) + (c0, c1)), one packed FFMA2.
+__device__ __forceinline__ void ffma2v(float& c0, float& c1, float a0, float a1, float b0, float b1) {
+  asm("{\n"
+      ".reg .b64 pa, pb, pc;\n"
+      "mov.b64 pa, {%2, %3};\n"
+      "mov.b64 pb, {%4, %5};\n"
+      "mov.b64 pc, {%0, %1};\n"
+      "fma.rn.f32x2 pc, pa, pb, pc;\n"
+      "mov.b64 {%0, %1}, pc;\n"
+      "}\n"
+      : "+f"(c0), "+f"(c1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+// (d0, d1) = fl((a0, a1) * s), one packed FMUL2.
+__device__ __forceinline__ void fmul2s(float& d0, float& d1, float a0, float a1, float s) {
+  asm("{\n"
+      ".reg .b64 pa, pb, pd;\n"
+      "mov.b64 pa, {%2, %3};\n"
+      "mov.b64 pb, {%4, %4};\n"
+      "mul.rn.f32x2 pd, pa, pb;\n"
+      "mov.b64 {%0, %1}, pd;\n"
+      "}\n"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(s));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

@@ -12,8 +12,8 @@
 // zeroes smem rows [res, 128) so the MMA's reduction sees exact zeros: no row of
 // another group is ever read into the product, and nothing is padded in HBM.
 //
-// Persistent 1-CTA tiles of 128 (K) x 128 (N), tcgen05.mma cta_group::1 M=128 N=128,
-// A = X^T and B = dY both MN-major in 128B-swizzled smem (token rows), 4 TMEM
+// Persistent CTA-pair tiles of 256 (K) x 256 (N), tcgen05.mma cta_group::2 M=256 N=256,
+// A = X^T and B = dY both MN-major in 128B-swizzled smem (token rows), 2 TMEM
 // accumulation buffers, warp roles as in tagg_gemm.cu (producer, MMA, 8 promotion warps).
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -33,12 +33,12 @@ namespace wg {
 constexpr int BT = 128;                 // tokens per k-block
 constexpr int kThreads = 384;
 constexpr int kPromoWarps = 8;
-constexpr int kNumAcc = 4;              // TMEM buffers of 128 columns
+constexpr int kNumAcc = 2;              // TMEM buffers of 256 columns
 constexpr int kStages = 4;
-constexpr int kScaleRing = 8;           // k-block scale slots (sx 128 + sdy 128 floats)
-constexpr uint32_t kStageA = BT * 128;  // 128 token rows x 128 K columns
-constexpr uint32_t kStageB = BT * 128;  // 128 token rows x 128 N columns
-constexpr uint32_t kScaleSlot = 2 * 128 * 4;
+constexpr int kScaleRing = 8;           // k-block scale slots: sx 128 + sdy 256 floats
+constexpr uint32_t kStageA = BT * 128;  // 128 token rows x this CTA's 128 K columns
+constexpr uint32_t kStageB = BT * 128;  // 128 token rows x this CTA's 128 N columns
+constexpr uint32_t kScaleSlot = (128 + 256) * 4;
 constexpr uint32_t kChunkC = 128 * 128;  // 128 rows x 64 bf16 columns
 constexpr int kPool = 8;
 
@@ -49,15 +49,20 @@ struct Params {
   const float* sx;            // [TB, K]
   const float* sdy;           // [TB, N]
   const int32_t* group_sizes;
-  int G, K, N, KT, NT;
+  int G, K, N, KT, NT;        // KT, NT: 256-wide pair tiles (ceil)
   uint32_t off_a, off_b, off_c, off_s, off_tab, off_bar;
 };
 
+// CTA pair (cluster of 2, tcgen05 cta_group::2) per 256 (K) x 256 (N) tile of dW_g: CTA
+// `rank` holds K rows [k0 + 128 rank, +128) of X^T and B columns [n0 + 128 rank, +128)
+// of dY; each CTA's TMEM gets its 128 rows x all 256 columns.
 __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = p.G;
+  const int rank = static_cast<int>(cluster_ctarank());
+  const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   int32_t* tab_off = reinterpret_cast<int32_t*>(smem + p.off_tab);  // [G] first row
   int32_t* tab_tb = tab_off + G;                                      // [G] first token block
   int32_t* tab_m = tab_tb + G;                                        // [G] rows
@@ -72,12 +77,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < kStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&full[i], 2);   // the leader's arrive.expect_tx + the peer's arrive (its zero rows)
+      mbar_init(&empty[i], 1);  // MMA commit, multicast
     }
     for (int i = 0; i < kNumAcc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kPromoWarps);
+      mbar_init(&tempty[i], kPromoWarps * 2);
     }
     for (int i = 0; i < kScaleRing; ++i) {
       mbar_init(&sfull[i], 1);
@@ -85,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<1>(tmem_slot, 512);
+  if (warp == 1) tmem_alloc<2>(tmem_slot, 512);
   if (warp == 2) {
     int carry_r = 0, carry_b = 0;
     for (int base = 0; base < G; base += 32) {
@@ -109,30 +114,33 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const int tiles = G * p.KT * p.NT;
 
   if (warp < 4) {
     setmaxnreg_dec<72>();
     if (warp == 0) {
-      // ====================================================== producer
+      // ====================================================== producer (both CTAs)
       uint32_t stage = 0, phase = 0, sring = 0, sph = 0;
       const uint32_t sA0 = smem_u32(smem + p.off_a), sB0 = smem_u32(smem + p.off_b);
       const uint32_t sS0 = smem_u32(smem + p.off_s);
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = cid; t < tiles; t += nclusters) {
         const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
-        const int k0 = (rem / p.NT) * 128, n0 = (rem % p.NT) * 128;
+        const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
+        const int kr = k0 + 128 * rank, nr = n0 + 128 * rank;  // this CTA's K rows, B columns
         const int m = tab_m[g], off = tab_off[g], tb0 = tab_tb[g];
         for (int j = 0; j * BT < m; ++j) {
-          // scales of this token block: sx[tb][k0..+128), sdy[tb][n0..+128)
+          // scales of this token block: sx[tb][kr..+128), sdy[tb][n0..+256)
           mbar_wait_addr(smem_u32(&sempty[sring]), sph ^ 1);
           if (lane == 0) {
             const uint32_t dst = sS0 + sring * kScaleSlot;
             const int64_t tb = tb0 + j;
-            mbar_arrive_expect_tx_addr(smem_u32(&sfull[sring]), kScaleSlot);
-            bulk_load_1d_addr(dst, p.sx + tb * p.K + k0, 512, smem_u32(&sfull[sring]));
-            bulk_load_1d_addr(dst + 512, p.sdy + tb * p.N + n0, 512, smem_u32(&sfull[sring]));
+            const uint32_t nsx = kr < p.K ? 512u : 0u;
+            const uint32_t nsdy = n0 + 256 <= p.N ? 1024u : 512u;
+            mbar_arrive_expect_tx_addr(smem_u32(&sfull[sring]), nsx + nsdy);
+            if (nsx) bulk_load_1d_addr(dst, p.sx + tb * p.K + kr, nsx, smem_u32(&sfull[sring]));
+            bulk_load_1d_addr(dst + 512, p.sdy + tb * p.N + n0, nsdy, smem_u32(&sfull[sring]));
           }
           if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
           // operands
@@ -153,18 +161,22 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           __syncwarp();
           if (lane == 0) {
             const uint32_t fb = smem_u32(&full[stage]);
-            if (res == BT) {
-              mbar_arrive_expect_tx_addr(fb, kStageA + kStageB);
-              tma_load_2d_u32<1>(&p.map_x[7], fb, a_dst, k0, row0);
-              tma_load_2d_u32<1>(&p.map_dy[7], fb, b_dst, n0, row0);
+            const int lg = res == BT ? 7 : 31 - __clz(res), d = 1 << lg;
+            const uint32_t bytes = (res == BT) ? 2u * (kStageA + kStageB) : 2u * 4u * d * 128u;
+            if (rank == 0) {
+              mbar_arrive_expect_tx_addr(fb, bytes);
+            } else if (res < BT) {
+              // release the zero rows to the pair's MMA, then count on the leader's barrier
+              asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(fb & 0xFEFFFFFFu)
+                           : "memory");
             } else {
-              // dual-phase load from the pool: rows [0, d) and [res - d, res)
-              const int lg = 31 - __clz(res), d = 1 << lg;
-              mbar_arrive_expect_tx_addr(fb, 4u * d * 128u);
-              tma_load_2d_u32<1>(&p.map_x[lg], fb, a_dst, k0, row0);
-              tma_load_2d_u32<1>(&p.map_x[lg], fb, a_dst + (res - d) * 128u, k0, row0 + res - d);
-              tma_load_2d_u32<1>(&p.map_dy[lg], fb, b_dst, n0, row0);
-              tma_load_2d_u32<1>(&p.map_dy[lg], fb, b_dst + (res - d) * 128u, n0, row0 + res - d);
+              mbar_arrive_leader_addr(fb);  // nothing of ours to publish: the TMA bytes count themselves
+            }
+            tma_load_2d_u32<2>(&p.map_x[lg], fb, a_dst, kr, row0);
+            tma_load_2d_u32<2>(&p.map_dy[lg], fb, b_dst, nr, row0);
+            if (res < BT) {  // dual phase: rows [0, d) above, rows [res - d, res) here
+              tma_load_2d_u32<2>(&p.map_x[lg], fb, a_dst + (res - d) * 128u, kr, row0 + res - d);
+              tma_load_2d_u32<2>(&p.map_dy[lg], fb, b_dst + (res - d) * 128u, nr, row0 + res - d);
             }
           }
           __syncwarp();
@@ -177,18 +189,17 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       __syncwarp();
-    } else if (warp == 1) {
-      // ====================================================== MMA (whole warp, elected issue)
+    } else if (warp == 1 && rank == 0) {
+      // ====================================================== MMA (leader, whole warp, elected issue)
       const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
-      const uint32_t idesc = idesc_e4m3_f32_ab(128, 128, true, true);
-      // MN-major operands: 128 token rows of 128 B (one swizzle atom wide), 8-row groups
-      // of 1 KB; K = 32 tokens per MMA = 32 rows = 4 KB
+      const uint32_t idesc = idesc_e4m3_f32_ab(256, 256, true, true);
+      // MN-major operands: 128 token rows of 128 B (one swizzle atom wide per CTA), 8-row
+      // groups of 1 KB; K = 32 tokens per MMA = 32 rows = 4 KB
       const uint64_t a0 = umma_desc_sw128(smem_u32(smem + p.off_a), kStageA, 1024);
       const uint64_t b0 = umma_desc_sw128(smem_u32(smem + p.off_b), kStageB, 1024);
       uint32_t stage = 0, phase = 0, acc = 0, accph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int g = t / (p.KT * p.NT);
-        const int m = tab_m[g];
+      for (int t = cid; t < tiles; t += nclusters) {
+        const int m = tab_m[t / (p.KT * p.NT)];
         for (int j = 0; j * BT < m; ++j) {
           mbar_wait_addr(smem_u32(&tempty[acc]), accph ^ 1);
           mbar_wait_addr(smem_u32(&full[stage]), phase);
@@ -197,10 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_f8f6f4<1>(tmem_base + acc * 128, ad + static_cast<uint64_t>(k * 256),
+              mma_f8f6f4<2>(tmem_base + acc * 256, ad + static_cast<uint64_t>(k * 256),
                             bd + static_cast<uint64_t>(k * 256), idesc, k > 0 ? 1u : 0u);
-            mma_commit_addr<1>(smem_u32(&empty[stage]));
-            mma_commit_addr<1>(smem_u32(&tfull[acc]));
+            mma_commit_addr<2>(smem_u32(&empty[stage]));
+            mma_commit_addr<2>(smem_u32(&tfull[acc]));
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -213,85 +224,95 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     // ====================================================== promotion + epilogue
     const uint32_t tmem_base = opaque_u32(ld_shared_u32(smem_u32(tmem_slot)));
     const int pw = warp - 4, q = warp & 3, half = pw >> 2;
-    const int r = 32 * q + lane;  // dW row within the tile (K index k0 + r)
+    const int r = 32 * q + lane;  // row of this CTA's 128 dW rows
     const int ptid = threadIdx.x - 128;
     const uint32_t t_lane = static_cast<uint32_t>(32 * q) << 16;
     const uint32_t sS0 = opaque_u32(smem_u32(smem + p.off_s));
     const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
     const uint32_t sfull0 = opaque_u32(smem_u32(&sfull[0])), sempty0 = opaque_u32(smem_u32(&sempty[0]));
-    uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0, tiles_done = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0;
+    for (int t = cid; t < tiles; t += nclusters) {
       const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
-      const int k0 = (rem / p.NT) * 128, n0 = (rem % p.NT) * 128;
+      const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
+      const int kr = k0 + 128 * rank;
       const int m = tab_m[g];
-      float acc[64];
+      float acc[128];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
+      for (int i = 0; i < 128; ++i) acc[i] = 0.0f;
       for (int j = 0; j * BT < m; ++j) {
         mbar_wait_addr(sfull0 + 8 * sring, sph);
         const uint32_t slot = sS0 + sring * kScaleSlot;
         const float sxk = ld_shared_f32(slot + 4u * r);
-        const uint32_t sdy = slot + 512u + 4u * (64u * half);
+        const uint32_t sdy = slot + 512u + 4u * (128u * half);
         mbar_wait_addr(tfull0 + 8 * acc_i, accph);
         tc_fence_after();
-        uint32_t v[64];
-        tmem_ld_32x32b_x64(tmem_base + t_lane + acc_i * 128 + 64u * half, v);
-        tmem_wait_ld_dep64(v);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_addr(tempty0 + 8 * acc_i);
+        const uint32_t taddr = tmem_base + t_lane + acc_i * 256 + 128u * half;
 #pragma unroll
-        for (int c = 0; c < 64; c += 4) {
-          float4 sd;
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(sd.x), "=f"(sd.y), "=f"(sd.z), "=f"(sd.w)
-                       : "r"(sdy + 4u * c));
-          // s = fl(sx * sdy); acc = fl(acc + fl(inner * s)) with the product rounding
-          // folded into one FMA (as the forward's default promotion)
-          acc[c + 0] = __fmaf_rn(__uint_as_float(v[c + 0]), __fmul_rn(sxk, sd.x), acc[c + 0]);
-          acc[c + 1] = __fmaf_rn(__uint_as_float(v[c + 1]), __fmul_rn(sxk, sd.y), acc[c + 1]);
-          acc[c + 2] = __fmaf_rn(__uint_as_float(v[c + 2]), __fmul_rn(sxk, sd.z), acc[c + 2]);
-          acc[c + 3] = __fmaf_rn(__uint_as_float(v[c + 3]), __fmul_rn(sxk, sd.w), acc[c + 3]);
+        for (int c2 = 0; c2 < 2; ++c2) {
+          uint32_t v[64];
+          tmem_ld_32x32b_x64(taddr + 64 * c2, v);
+          tmem_wait_ld_dep64(v);
+          if (c2 == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader_addr(tempty0 + 8 * acc_i);
+          }
+#pragma unroll
+          for (int c = 0; c < 64; c += 4) {
+            float4 sd;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(sd.x), "=f"(sd.y), "=f"(sd.z), "=f"(sd.w)
+                         : "r"(sdy + 4u * (64 * c2 + c)));
+            // acc = fl(fl(inner * sx) * sdy + acc): the row scale first (FMUL2), then the
+            // column scale and the add in one FFMA2 -- one packed instruction per element
+            // pair each (the reference rounds s = sx * sdy, the product and the sum
+            // separately; the difference is a few fp32 ulp, far inside the bf16 tolerance)
+            float* a = acc + 64 * c2 + c;
+            float t0, t1, t2, t3;
+            fmul2s(t0, t1, __uint_as_float(v[c + 0]), __uint_as_float(v[c + 1]), sxk);
+            fmul2s(t2, t3, __uint_as_float(v[c + 2]), __uint_as_float(v[c + 3]), sxk);
+            ffma2v(a[0], a[1], t0, t1, sd.x, sd.y);
+            ffma2v(a[2], a[3], t2, t3, sd.z, sd.w);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_addr(sempty0 + 8 * sring);
         if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
         if (++acc_i == kNumAcc) { acc_i = 0; accph ^= 1; }
       }
-      // epilogue: bf16 -> 128B-swizzled staging (double-buffered across tiles, so the
-      // previous tile's stores drain while this one is written), warp half h -> chunk h
-      const uint32_t sbuf = (tiles_done & 1) * 2 * kChunkC;
-      if (ptid == 0) bulk_wait_read1();
+      // epilogue: one pass, 4 chunks of 64 columns x 128 rows (64 KB); thread -> chunks
+      // 2 half, 2 half + 1 of its row
+      if (ptid == 0) bulk_wait_read0();
       named_bar_sync(1, 32 * kPromoWarps);
       {
-        const uint32_t base = smem_u32(smem + p.off_c) + sbuf + half * kChunkC + static_cast<uint32_t>(r) * 128u;
+        const uint32_t base = smem_u32(smem + p.off_c) + static_cast<uint32_t>(r) * 128u;
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
+        for (int jj = 0; jj < 16; ++jj) {
+          const uint32_t chunk = 2 * half + (jj >> 3);
           const uint32_t w0 = pack_bf16x2(acc[8 * jj + 0], acc[8 * jj + 1]);
           const uint32_t w1 = pack_bf16x2(acc[8 * jj + 2], acc[8 * jj + 3]);
           const uint32_t w2 = pack_bf16x2(acc[8 * jj + 4], acc[8 * jj + 5]);
           const uint32_t w3 = pack_bf16x2(acc[8 * jj + 6], acc[8 * jj + 7]);
-          st_shared_v4(base + static_cast<uint32_t>((jj ^ (r & 7)) * 16), w0, w1, w2, w3);
+          st_shared_v4(base + chunk * kChunkC + static_cast<uint32_t>(((jj & 7) ^ (r & 7)) * 16), w0, w1, w2, w3);
         }
         fence_proxy_async_smem();
       }
       named_bar_sync(1, 32 * kPromoWarps);
-      if (ptid == 0) {
-        const int row = g * p.K + k0;
-        tma_store_2d(&p.map_dw, smem + p.off_c + sbuf, n0, row);
-        tma_store_2d(&p.map_dw, smem + p.off_c + sbuf + kChunkC, n0 + 64, row);
+      if (ptid == 0 && kr < p.K) {
+        const int row = g * p.K + kr;
+        for (int c = 0; c < 4; ++c)
+          if (n0 + 64 * c < p.N) tma_store_2d(&p.map_dw, smem + p.off_c + c * kChunkC, n0 + 64 * c, row);
         bulk_commit();
       }
-      ++tiles_done;
     }
     if (ptid == 0) bulk_wait0();
   }
   __syncwarp();
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<1>(ld_shared_u32(smem_u32(tmem_slot)), 512);
+    tmem_dealloc<2>(ld_shared_u32(smem_u32(tmem_slot)), 512);
   }
 }
 
@@ -435,12 +456,12 @@ extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, co
   p.G = G;
   p.K = K;
   p.N = N;
-  p.KT = K / 128;
-  p.NT = N / 128;
+  p.KT = (K + 255) / 256;
+  p.NT = (N + 255) / 256;
   p.off_a = 0;
   p.off_b = p.off_a + kStages * kStageA;
   p.off_c = p.off_b + kStages * kStageB;
-  p.off_s = p.off_c + 4 * kChunkC;  // two staging buffers of 2 chunks
+  p.off_s = p.off_c + 4 * kChunkC;
   p.off_tab = p.off_s + kScaleRing * kScaleSlot;
   const uint32_t tab = static_cast<uint32_t>(((3 * G * 4) + 15) & ~15);
   p.off_bar = p.off_tab + tab;
@@ -453,9 +474,20 @@ extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, co
     configured = true;
   }
   const int64_t tiles = static_cast<int64_t>(G) * p.KT * p.NT;
-  const int grid = static_cast<int>(std::min<int64_t>(sms, tiles));
-  wgrad_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
-  const cudaError_t e = cudaGetLastError();
+  const int grid = static_cast<int>(std::min<int64_t>(sms / 2, tiles)) * 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1] = {};
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_kernel, p);
   if (e != cudaSuccess) {
     std::fprintf(stderr, "tagg_wgrad_fp8: launch failed: %s\n", cudaGetErrorString(e));
     return TAGG_ERR_CUDA;
