@@ -55,6 +55,11 @@ extern "C" {
 #define TAGG_FLAG_TILE_N128 8u       /* CTA-pair tile 256x128 (more, smaller tiles: fewer idle SMs
                                         in the last wave of small problems) */
 #define TAGG_FLAG_TILE_N256 16u      /* CTA-pair tile 256x256 (the default) */
+/* Cap the persistent grid at n SMs (flags bits 16-27; 0 = every SM).  An overlapped
+   expert-parallel exchange leaves the rest to the NCCL kernels that run beside the GEMM. */
+#define TAGG_SM_LIMIT_SHIFT 16
+#define TAGG_SM_LIMIT_MASK 0xFFFu
+#define TAGG_SM_LIMIT(n) (((uint32_t)(n) & TAGG_SM_LIMIT_MASK) << TAGG_SM_LIMIT_SHIFT)
 
 #define TAGG_TILE_MAP_FIELDS 9
 

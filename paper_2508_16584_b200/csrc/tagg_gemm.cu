@@ -902,11 +902,23 @@ static int tagg_launch_clusters_impl(int sms, int64_t m_alloc, int G, int N, int
   return static_cast<int>(std::min<int64_t>(sms / cg, std::max<int64_t>(bound, 1)));
 }
 
+// SMs a launch may occupy: the device's count, or the TAGG_SM_LIMIT(n) cap in flags bits
+// 16-27 (leaves SMs free for kernels that must co-run, e.g. NCCL during an overlapped
+// expert-parallel exchange).  0 = invalid cap (smaller than one cluster).
+static int launch_sms(uint32_t flags, int cg) {
+  const int sms = num_sms_for_current_device();
+  if (sms <= 0) return -1;
+  const int cap = static_cast<int>((flags >> TAGG_SM_LIMIT_SHIFT) & TAGG_SM_LIMIT_MASK);
+  if (cap == 0) return sms;
+  return cap < cg ? 0 : std::min(sms, cap);
+}
+
 extern "C" int tagg_launch_clusters(int64_t m_alloc, int G, int N, uint32_t flags) {
   if (m_alloc < 0 || G < 1 || N < 64) return TAGG_ERR_CONFIG;
-  const int sms = num_sms_for_current_device();
-  if (sms <= 0) return TAGG_ERR_CUDA;
   const int cg = (flags & TAGG_FLAG_SINGLE_CTA) ? 1 : 2;
+  const int sms = launch_sms(flags, cg);
+  if (sms < 0) return TAGG_ERR_CUDA;
+  if (sms == 0) return TAGG_ERR_CONFIG;
   const int bn = (cg == 1 || (flags & TAGG_FLAG_TILE_N128)) ? 128 : 256;
   return tagg_launch_clusters_impl(sms, m_alloc, G, N, cg, bn);
 }
@@ -938,8 +950,6 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   if (m_alloc == 0 || c_rows == 0) return TAGG_OK;  // nothing can be stored
   if (m_alloc >= (int64_t(1) << 31) || c_rows >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
 
-  const int sms = num_sms_for_current_device();
-  if (sms <= 0) return TAGG_ERR_CUDA;
   // ---- tile shape: the CTA-pair 256x256 tile by default (half the operand
   // traffic per FLOP of 256x128; measured faster even on the residual sweep,
   // whose 320 pair tiles leave the last of 5 waves 32% full), or an explicit
@@ -951,6 +961,9 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   } else if (flags & TAGG_FLAG_TILE_N128) {
     bn = 128;
   }
+  const int sms = launch_sms(flags, cg);
+  if (sms < 0) return TAGG_ERR_CUDA;
+  if (sms == 0) return TAGG_ERR_CONFIG;
   const int num_acc = 512 / bn;
   const uint32_t stage_bytes_b = static_cast<uint32_t>(BK * (bn / cg));
   const int kb_count = (K + BK - 1) / BK;

@@ -25,6 +25,7 @@ single-process.
 
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 
 import torch
@@ -134,6 +135,166 @@ def combine(c_local: torch.Tensor, meta: DispatchMeta, group=None) -> torch.Tens
     dist.all_to_all_single(out_sorted, c_recv_order, meta.send_splits, meta.recv_splits, group=group)
     out = torch.empty_like(out_sorted)
     out.index_copy_(0, meta.order, out_sorted)
+    return out
+
+
+# ---------------------------------------------------------------------------------------------
+# Overlapped dispatch -> GEMM -> combine
+
+
+@dataclass
+class ChunkPlan:
+    """Exchange plan for C row chunks, built with ONE count all-to-all and ONE host read.
+
+    Local rows are split into C contiguous chunks and stably sorted by (chunk, expert);
+    chunk c's rows then sit at sorted positions [send_off[c], send_off[c+1]), grouped by
+    destination rank because experts are rank-contiguous.
+    """
+
+    chunks: int
+    order: torch.Tensor            # sorted position -> local row (int64 [R])
+    send_splits: list              # [C][P] rows of chunk c sent to rank p
+    recv_splits: list              # [C][P] rows of chunk c received from rank p
+    send_off: list                 # [C+1] chunk offsets in the sorted send buffer
+    to_grouped: list               # [C] received-row index of each grouped row (int64 device)
+    group_sizes: list              # [C] int32 [E_local] device group sizes of chunk c
+    experts_per_rank: int
+
+    @property
+    def recv_rows(self) -> list:
+        return [sum(r) for r in self.recv_splits]
+
+
+def _regroup_index(recv_mat: torch.Tensor, n_recv: int) -> torch.Tensor:
+    """Received rows arrive (src rank, expert)-ordered; index them in (expert, src) order."""
+    world, epr = recv_mat.shape
+    dev = recv_mat.device
+    flat = recv_mat.reshape(-1).to(torch.int64)
+    src_off = (torch.cumsum(flat, 0) - flat).view(world, epr)
+    seg_len = recv_mat.t().reshape(-1).to(torch.int64)
+    seg_start = src_off.t().reshape(-1)
+    seg_dst = torch.cumsum(seg_len, 0) - seg_len
+    idx = torch.arange(n_recv, device=dev, dtype=torch.int64)
+    seg_of = torch.repeat_interleave(torch.arange(seg_len.numel(), device=dev), seg_len, output_size=n_recv)
+    return seg_start[seg_of] + (idx - seg_dst[seg_of])
+
+
+def plan_chunks(expert_ids: torch.Tensor, num_experts: int, chunks: int, group=None) -> ChunkPlan:
+    """Sort R routed rows by (chunk, expert) and exchange every chunk's counts at once."""
+    world = dist.get_world_size(group)
+    if num_experts % world:
+        raise ValueError(f"{num_experts} experts do not split over {world} ranks")
+    if chunks < 1:
+        raise ValueError("chunks must be >= 1")
+    epr = num_experts // world
+    ids = expert_ids.reshape(-1).to(torch.int64)
+    rows = ids.numel()
+    dev = ids.device
+    chunk_of = torch.arange(rows, device=dev, dtype=torch.int64) * chunks // max(rows, 1)
+    key = chunk_of * num_experts + ids
+    order = torch.argsort(key, stable=True)
+    counts = torch.bincount(key, minlength=chunks * num_experts).to(torch.int32).view(chunks, world, epr)
+    send = counts.permute(1, 0, 2).contiguous()                    # [dst rank, chunk, local expert]
+    recv = torch.empty_like(send)                                   # [src rank, chunk, local expert]
+    dist.all_to_all_single(recv, send, group=group)
+    both = torch.cat([counts.sum(2).reshape(-1), recv.sum(2).t().reshape(-1)]).cpu().tolist()  # one sync
+    n = chunks * world
+    send_splits = [both[c * world:(c + 1) * world] for c in range(chunks)]
+    recv_splits = [both[n + c * world:n + (c + 1) * world] for c in range(chunks)]
+    send_off = [0]
+    for c in range(chunks):
+        send_off.append(send_off[-1] + sum(send_splits[c]))
+    to_grouped = [_regroup_index(recv[:, c, :], sum(recv_splits[c])) for c in range(chunks)]
+    group_sizes = [recv[:, c, :].sum(0).to(torch.int32) for c in range(chunks)]
+    return ChunkPlan(chunks, order, send_splits, recv_splits, send_off, to_grouped, group_sizes, epr)
+
+
+def pipelined_expert_gemm(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_ids: torch.Tensor,
+                          num_experts: int, expert_gemm, n_out: int, *, chunks: int = 4, group=None,
+                          comm_stream=None, out_dtype=torch.bfloat16, plan: ChunkPlan | None = None):
+    """Dispatch -> per-expert GEMM -> combine, pipelined over row chunks.
+
+    a_codes [R, K] e4m3 codes, a_scales [R, kb] f32 and expert_ids [R] are this rank's routed
+    rows (dispatch() semantics).  ``expert_gemm(codes, scales, group_sizes) -> [rows, n_out]``
+    runs this rank's experts on one chunk's rows in the padding-free grouped layout (codes may
+    be a row-strided view).  Returns [R, n_out]: every row's output back in local row order.
+
+    Codes and scales travel packed in one all-to-all per chunk (K + 4*kb bytes a row, padded
+    to 16).  On CUDA
+    the all-to-alls run on ``comm_stream``: chunk c's GEMM overlaps chunk c+1's dispatch and
+    chunk c-1's combine.  Give the GEMM fewer SMs than the device has (grouped_gemm_fp8
+    ``max_sms``) so the NCCL kernels find room beside its persistent grid.
+    """
+    if a_codes.dtype == torch.float8_e4m3fn:
+        a_codes = a_codes.view(torch.uint8)
+    rows, k = a_codes.shape
+    kb = a_scales.shape[1]
+    dev = a_codes.device
+    if plan is None:
+        plan = plan_chunks(expert_ids, num_experts, chunks, group)
+    width = -(-(k + 4 * kb) // 16) * 16     # 16-byte rows: the GEMM's TMA reads codes in place
+    packed = torch.empty((rows, width), dtype=torch.uint8, device=dev)
+    packed[:, :k] = a_codes.index_select(0, plan.order)
+    packed[:, k:k + 4 * kb] = a_scales.contiguous().index_select(0, plan.order).view(torch.uint8)
+    out_sorted = torch.empty((rows, n_out), dtype=out_dtype, device=dev)
+    cuda = dev.type == "cuda"
+    compute = torch.cuda.current_stream(dev) if cuda else None
+    comm = (comm_stream or torch.cuda.Stream(dev)) if cuda else None
+
+    def on(stream):
+        return torch.cuda.stream(stream) if cuda else contextlib.nullcontext()
+
+    def event():
+        return torch.cuda.Event() if cuda else None
+
+    if cuda:
+        comm.wait_stream(compute)                                    # the packed rows
+    recv = [None] * plan.chunks
+    arrived = [event() for _ in range(plan.chunks)]
+    done = [event() for _ in range(plan.chunks)]
+    back = [None] * plan.chunks
+
+    def send_chunk(c):
+        with on(comm):
+            recv[c] = torch.empty((plan.recv_rows[c], width), dtype=torch.uint8, device=dev)
+            lo, hi = plan.send_off[c], plan.send_off[c + 1]
+            dist.all_to_all_single(recv[c], packed[lo:hi], plan.recv_splits[c], plan.send_splits[c], group=group)
+            if cuda:
+                arrived[c].record(comm)
+
+    def return_chunk(c):
+        with on(comm):
+            if cuda:
+                comm.wait_event(done[c])
+            lo, hi = plan.send_off[c], plan.send_off[c + 1]
+            dist.all_to_all_single(out_sorted[lo:hi], back[c], plan.send_splits[c], plan.recv_splits[c],
+                                   group=group)
+
+    send_chunk(0)
+    for c in range(plan.chunks):
+        if cuda:
+            compute.wait_event(arrived[c])
+        n = plan.recv_rows[c]
+        grouped = recv[c].index_select(0, plan.to_grouped[c])        # padding-free grouped layout
+        y = (expert_gemm(grouped[:, :k], grouped[:, k:k + 4 * kb].contiguous().view(torch.float32),
+                         plan.group_sizes[c])
+             if n else torch.empty((0, n_out), dtype=out_dtype, device=dev))
+        back[c] = torch.empty((n, n_out), dtype=out_dtype, device=dev)
+        back[c].index_copy_(0, plan.to_grouped[c], y[:n])
+        if cuda:
+            done[c].record(compute)
+            # the comm stream's allocations are used by compute too
+            recv[c].record_stream(compute)
+            back[c].record_stream(comm)
+        if c + 1 < plan.chunks:
+            send_chunk(c + 1)                                         # ahead of combine(c): GEMM c+1 needs it
+        return_chunk(c)
+    if cuda:
+        compute.wait_stream(comm)
+        packed.record_stream(comm)
+        out_sorted.record_stream(comm)
+    out = torch.empty_like(out_sorted)
+    out.index_copy_(0, plan.order, out_sorted)
     return out
 
 

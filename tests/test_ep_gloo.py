@@ -82,3 +82,54 @@ def test_dispatch_combine_world2(rows_per_rank, experts):
         p.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
     assert sum(n for _, _, n in res) == sum(rows_per_rank)
+
+
+def _pipeline_worker(rank, world, port, rows_per_rank, k, experts, chunks, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, sa, e = _inputs(rank, rows_per_rank[rank], k, experts, seed)
+        epr = experts // world
+        seen = []
+
+        def fake_gemm(codes, scales, gs):
+            """Stand-in for the grouped GEMM: echoes each row's first codes, its local expert
+            (read off the group sizes, so it only matches if rows arrive grouped) and scale."""
+            seen.append(gs.clone())
+            local_e = torch.repeat_interleave(torch.arange(epr), gs.to(torch.int64))
+            return torch.cat([codes[:, :4].to(torch.float32), local_e[:, None].to(torch.float32),
+                              scales[:, :1]], 1)
+
+        out = ep.pipelined_expert_gemm(a, sa, e, experts, fake_gemm, 6, chunks=chunks, out_dtype=torch.float32)
+        want = torch.cat([a[:, :4].to(torch.float32), (e % epr)[:, None].to(torch.float32), sa[:, :1]], 1)
+        ok = out.shape == want.shape and torch.equal(out, want)
+        # every chunk's GEMM got exactly that chunk's rows for my experts
+        sl = ep.local_expert_slice(experts)
+        total = torch.zeros(epr, dtype=torch.int64)
+        for gs in seen:
+            total += gs.to(torch.int64)
+        want_total = torch.zeros(epr, dtype=torch.int64)
+        for src in range(world):
+            _, _, e2 = _inputs(src, rows_per_rank[src], k, experts, seed)
+            want_total += torch.bincount(e2[(e2 >= sl.start) & (e2 < sl.stop)] - sl.start, minlength=epr)
+        ok = ok and torch.equal(total, want_total)
+        q.put((rank, bool(ok), len(seen)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rows_per_rank,experts,chunks", [((300, 170), 8, 3), ((1, 0), 4, 2)])
+def test_pipelined_expert_gemm_world2(rows_per_rank, experts, chunks):
+    """Chunked dispatch -> expert GEMM -> combine returns every row's result home, in order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, 2, port, rows_per_rank, 384, experts, chunks, 5, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _ in res), res

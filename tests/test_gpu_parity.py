@@ -243,3 +243,31 @@ def test_identical_fraction_reported_for_reference_recipe():
         print(f"c1 exact={exact}: {rep}")
         assert rep["out_of_tol"] == 0
         assert rep["bit_identical"] > 0.9
+
+
+@pytest.mark.parametrize("max_sms", [2, 22, 132])
+@pytest.mark.parametrize("tile", ["1cta", "pair_n256"])
+def test_sm_limited_grid(max_sms, tile):
+    """TAGG_SM_LIMIT(n) caps the persistent grid (room for NCCL beside the GEMM): values and
+    the tile map (whose tail balancing depends on the cluster count) stay exact."""
+    from paper_2508_16584_b200._lib import lib
+
+    sizes = (700, 3, 129, 0, 1000, 255)
+    n, k = 768, 384
+    ac, asc, bc, bsc = _synthetic(sizes, n, k, max_sms)
+    m = sum(sizes)
+    flags = (4 if tile == "1cta" else 16) | (max_sms << 16)
+    clusters = lib().tagg_launch_clusters(m, len(sizes), n, flags)
+    assert 0 < clusters * (1 if tile == "1cta" else 2) <= max_sms
+    tmap = torch.full((tg.max_tiles(m, len(sizes), n), 9), -1, dtype=torch.int32, device=DEV)
+    out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
+                              tile=tile, tile_map=tmap, max_sms=max_sms)
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    assert_parity(got, oracle_c(ac, asc, bc, bsc, sizes), label=f"max_sms={max_sms}")
+    tm = tmap.cpu().numpy()
+    tm = sorted(tuple(int(x) for x in r) for r in tm[tm[:, 0] >= 0])
+    assert tm == sorted(oplan.kernel_tile_map(sizes, n, tile, num_pairs=clusters))
+    if tile == "pair_n256":
+        with pytest.raises(tg.ConfigError):
+            tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
+                                tile=tile, max_sms=1)
