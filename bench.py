@@ -174,6 +174,14 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- timing helpers
+def _free_port():
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def _timed_steps(torch, dist, world, step_fn, steps, warmup):
     for _ in range(warmup):
         step_fn()
@@ -315,6 +323,8 @@ def main():
     ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--exact", action="store_true", help="two-rounding promotion (TAGG_FLAG_EXACT_PROMOTION)")
+    ap.add_argument("--ep1", action="store_true",
+                    help="also run the DeepSeek-V3 down EP config (sequential vs overlapped) at one GPU")
     ap.add_argument("--profile-once", action="store_true", help="one step only (for ncu launch lists)")
     args = ap.parse_args()
 
@@ -428,7 +438,11 @@ def main():
             extra = run_extra(torch, tg, dev, rank, fp8_peak, args.exact)
         except Exception as exc:  # noqa: BLE001
             extra = {"error": f"{type(exc).__name__}: {exc}"}
-    if world > 1:
+    if world == 1 and args.ep1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    if world > 1 or args.ep1:
         try:
             extra["deepseek_v3_down_ep"] = run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, args.exact)
         except Exception as exc:  # noqa: BLE001
@@ -481,7 +495,7 @@ def main():
         "extra": extra,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -604,36 +618,68 @@ def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, war
             tg.grouped_gemm_fp8(state["a"], state["sa"], b, sb, state["meta"].group_sizes, out=state["out"],
                                 exact_promotion=exact)
 
+    def combine():
+        m = state["a"].shape[0]
+        state["back"] = ep.combine(state["out"][:m], state["meta"])
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    gemm_sms = sms - 16  # the overlapped path leaves 16 SMs to the NCCL kernels
+    chunks = 4
+
+    def capped(codes, scales, gs):
+        return tg.grouped_gemm_fp8(codes, scales, b, sb, gs, exact_promotion=exact, max_sms=gemm_sms)
+
+    def overlapped():
+        state["ov"] = ep.pipelined_expert_gemm(a, sa, eid, E, capped, N, chunks=chunks)
+
     for _ in range(warmup):
         dispatch()
         gemm()
+        combine()
+        overlapped()
     torch.cuda.synchronize()
     dist.barrier()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    t_a2a = t_gemm = 0.0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    t_a2a = t_gemm = t_comb = t_ov = 0.0
     for _ in range(iters):
         ev[0].record()
         dispatch()
         ev[1].record()
         gemm()
         ev[2].record()
+        combine()
+        ev[3].record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev[4].record()
+        overlapped()
+        ev[5].record()
         torch.cuda.synchronize()
         t_a2a += ev[0].elapsed_time(ev[1])
         t_gemm += ev[1].elapsed_time(ev[2])
+        t_comb += ev[2].elapsed_time(ev[3])
+        t_ov += ev[4].elapsed_time(ev[5])
+    same = bool(torch.equal(state["back"].view(torch.int16), state["ov"].view(torch.int16)))
     local_rows = state["a"].shape[0]
     flops_local = 2.0 * local_rows * N * K
-    stats = torch.tensor([t_a2a / iters, t_gemm / iters, flops_local, local_rows], dtype=torch.float64, device=dev)
+    stats = torch.tensor([t_a2a / iters, t_gemm / iters, flops_local, local_rows, t_comb / iters, t_ov / iters],
+                         dtype=torch.float64, device=dev)
     mx = stats.clone()
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     tot = stats.clone()
     dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    a2a_ms, gemm_ms = float(mx[0]), float(mx[1])
+    a2a_ms, gemm_ms, comb_ms, ov_ms = float(mx[0]), float(mx[1]), float(mx[4]), float(mx[5])
+    seq_ms = a2a_ms + gemm_ms + comb_ms
     return {"N": N, "K": K, "experts": E, "experts_per_rank": epr, "tokens": tokens, "topk": topk, "world": world,
             "rows_total": int(tot[3]), "rows_max_rank": int(mx[3]),
             "gemm_tflops_aggregate": float(tot[2]) / (gemm_ms * 1e-3) / 1e12,
             "gemm_tflops_per_gpu_max_rank": float(mx[2]) / (gemm_ms * 1e-3) / 1e12,
             "e2e_tflops_aggregate_incl_a2a": float(tot[2]) / ((gemm_ms + a2a_ms) * 1e-3) / 1e12,
-            "a2a_ms_max": a2a_ms, "gemm_ms_max": gemm_ms,
+            "a2a_ms_max": a2a_ms, "gemm_ms_max": gemm_ms, "combine_ms_max": comb_ms,
+            "sequential_dispatch_gemm_combine_ms": seq_ms,
+            "overlapped": {"ms": ov_ms, "chunks": chunks, "gemm_sms": gemm_sms,
+                           "tflops_aggregate": float(tot[2]) / (ov_ms * 1e-3) / 1e12,
+                           "speedup_vs_sequential": seq_ms / ov_ms, "bitwise_equal_to_sequential": same},
             "a2a_bytes_per_row": K + 4 * (K // 128), "transport": "NCCL all_to_all_single (NVLink/NVSwitch)"}
 
 
