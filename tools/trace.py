@@ -61,6 +61,9 @@ cases = [("sq8192", [(8192,)], 8192, 8192, 1), ("sweep_r64", [tuple(128 * g + 64
 if len(sys.argv) > 1 and sys.argv[1] == "ds":
     from bench import deepseek_gateup_sizes
     cases = [("ds", [tuple(int(x) for x in deepseek_gateup_sizes(0)[1])], 4096, 7168, 32)]
+if len(sys.argv) > 1 and sys.argv[1] == "dsdown":
+    from bench import deepseek_gateup_sizes
+    cases = [("dsdown", [tuple(int(x) for x in deepseek_gateup_sizes(seed=1)[0])], 7168, 2048, 256)]
 if len(sys.argv) > 1 and sys.argv[1] == "qdown":
     cases = [("qdown", [tuple([2048] * 128)], 4096, 1536, 128)]
 if len(sys.argv) > 1 and sys.argv[1] == "longk":
@@ -76,5 +79,5 @@ for name, sizes, n, k, G in cases:
         run(P, flags, G)
         torch.cuda.synchronize()
         L.tagg_debug_trace(None)
-        report(buf.cpu().numpy(), 8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60, "qdown": 600, "ds": 1000}[name], f"{name} {label}")
+        report(buf.cpu().numpy(), 8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60, "qdown": 600, "ds": 1000, "dsdown": 1000}[name], f"{name} {label}")
     del P
