@@ -67,7 +67,7 @@ def format_plan(plans) -> str:
     return "\n".join(lines)
 
 
-def kernel_tile_map(group_sizes, n: int, tile: str = "pair_n256", c_row_offsets=None, num_pairs=None):
+def kernel_tile_map(group_sizes, n: int, tile: str = "pair_n256", c_row_offsets=None, num_pairs=None, raster=8):
     """The store geometry the B200 kernel uses, stated with the reference planner.
 
     Every stored piece follows plan_two_phase (descriptors.py:72-106) for its block
@@ -94,15 +94,15 @@ def kernel_tile_map(group_sizes, n: int, tile: str = "pair_n256", c_row_offsets=
         o += rows
     ntn = -(-n // 256)
     # the kernel's static schedule (decode_tile): groups in order, inside a group
-    # super-rows of 8 pair m-tiles with n-tiles outer
+    # super-rows of `raster` pair m-tiles (tagg_raster_tiles) with n-tiles outer
     sched = []
     for g, rows in enumerate(sizes):
         pt = -(-rows // 256)
         for local in range(pt * ntn):
-            sr = local // (8 * ntn)
-            h = min(8, pt - sr * 8)
-            loc = local - sr * 8 * ntn
-            sched.append((g, sr * 8 + loc % h, (loc // h) * 256))
+            sr = local // (raster * ntn)
+            h = min(raster, pt - sr * raster)
+            loc = local - sr * raster * ntn
+            sched.append((g, sr * raster + loc % h, (loc // h) * 256))
     T = len(sched)
     x = 0
     if num_pairs:

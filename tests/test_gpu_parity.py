@@ -50,6 +50,7 @@ def _pairs(sizes, n):
     return lib().tagg_launch_clusters(int(sum(sizes)), len(sizes), n, 0)
 
 
+
 @pytest.mark.parametrize("name", CASES)
 @pytest.mark.parametrize("tile", ["1cta", "pair_n128", "pair_n256"])
 def test_tile_map_is_bit_exact(name, tile):
@@ -271,3 +272,25 @@ def test_sm_limited_grid(max_sms, tile):
         with pytest.raises(tg.ConfigError):
             tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
                                 tile=tile, max_sms=1)
+
+
+@pytest.mark.parametrize("max_sms", [0, 60])
+def test_tile_map_with_tall_groups_spanning_super_rows(max_sms):
+    """Groups taller than one raster super-row (8 pair m-tiles), with a tail split: the tile
+    map still equals the reference tile loop's store geometry."""
+    sizes = (8 * 256 * 5 + 77, 3, 300, 8 * 256 + 256)
+    n, k = 512, 256
+    ac, asc, bc, bsc = _synthetic(sizes, n, k, 31)
+    m = sum(sizes)
+    from paper_2508_16584_b200._lib import lib
+    clusters = lib().tagg_launch_clusters(m, len(sizes), n, max_sms << 16)
+    tmap = torch.full((tg.max_tiles(m, len(sizes), n), 9), -1, dtype=torch.int32, device=DEV)
+    out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
+                              tile_map=tmap, max_sms=max_sms or None)
+    tm = tmap.cpu().numpy()
+    tm = sorted(tuple(int(x) for x in r) for r in tm[tm[:, 0] >= 0])
+    assert tm == sorted(oplan.kernel_tile_map(sizes, n, "pair_n256", num_pairs=clusters))
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    want = np.zeros((m, n), dtype=np.uint16)
+    oracle_c(ac, asc, bc, bsc, sizes, n_range=(256, 384), out=want)
+    assert_parity(got[:, 256:384], want[:, 256:384], label="tall groups")

@@ -163,12 +163,13 @@ def test_tile_map_restatement_covers_rows_exactly():
 @pytest.mark.parametrize("sizes", [(1, 67, 128, 255, 0, 256, 129), (64, 65, 192, 320, 384, 3), (128 * 3 + 77,),
                                    tuple(128 * g + 64 for g in range(8))])
 @pytest.mark.parametrize("pairs", [None, 3, 74])
-def test_kernel_tile_map_stores_exactly_the_reference_rows(sizes, pairs):
+@pytest.mark.parametrize("raster", [1, 8, 64])
+def test_kernel_tile_map_stores_exactly_the_reference_rows(sizes, pairs, raster):
     """The kernel's half-tile pieces (64-row reference plans, group tails and the
     tail-balanced last wave) cover exactly the rows of the reference tile loop and
     never a row past M_g."""
     n = 512
-    ker = oplan.kernel_tile_map(sizes, n, num_pairs=pairs)
+    ker = oplan.kernel_tile_map(sizes, n, num_pairs=pairs, raster=raster)
     ref = oplan.tile_map(sizes, n)
     rows = lambda recs: sorted({(r[0], r[2], x) for r in recs for x in range(r[6], r[6] + r[4])})  # noqa: E731
     assert rows(ker) == rows(ref)

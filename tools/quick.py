@@ -30,7 +30,10 @@ shapes = [
     ("sweep_r64", [tuple(128 * g + 64 for g in range(8))], 4096, 7168, 8, "kn"),
     ("ds_gateup", [tuple(int(x) for x in deepseek_gateup_sizes(0)[1])], 4096, 7168, 32, "kn"),
     ("qwen_dgrad_gu", None, 4096, 3072, 128, "nk"),
+    ("ds_down", [tuple(int(x) for x in deepseek_gateup_sizes(seed=1)[0])], 7168, 2048, 256, "kn"),
 ]
+only = [a for a in args[1:]] if len(args) > 1 else None
+shapes = [s for s in shapes if only is None or s[0] in only]
 for name, sizes, n, k, G, bl in shapes:
     if sizes is None:
         sizes = [tuple([2048] * 128)]
