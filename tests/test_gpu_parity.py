@@ -294,3 +294,48 @@ def test_tile_map_with_tall_groups_spanning_super_rows(max_sms):
     want = np.zeros((m, n), dtype=np.uint16)
     oracle_c(ac, asc, bc, bsc, sizes, n_range=(256, 384), out=want)
     assert_parity(got[:, 256:384], want[:, 256:384], label="tall groups")
+
+
+def test_largest_k_and_the_unsupported_limit():
+    """K is bounded by the on-chip budget (two S_A windows of 128 rows x 4*ceil(K/128) bytes
+    beside two pipeline stages): every K <= 15872 fits (16128 is the largest that does), and
+    K = 16256 raises Unsupported before launch (tagg.h TAGG_ERR_UNSUPPORTED), never a wrong
+    result."""
+    sizes = (130, 1, 256)
+    n = 128
+    for k in (15872, 16128, 16256):
+        ac, asc, bc, bsc = _synthetic(sizes, n, k, k)
+        args = (_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)))
+        if k == 16256:
+            with pytest.raises(tg.Unsupported):
+                tg.grouped_gemm_fp8(*args)
+            continue
+        for tile in ("1cta", "pair_n256"):
+            got = tg.grouped_gemm_fp8(*args, tile=tile).view(torch.int16).cpu().numpy().view(np.uint16)
+            assert_parity(got, oracle_c(ac, asc, bc, bsc, sizes), label=f"k={k} {tile}")
+
+
+def test_thousands_of_groups_mostly_empty():
+    """G = 4096 experts (device group tables in smem), 95% of them empty, ragged rest."""
+    rng = np.random.default_rng(4096)
+    sizes = tuple(int(x) if rng.random() < 0.05 else 0 for x in rng.integers(1, 300, 4096))
+    n, k = 128, 256
+    ac, asc, bc, bsc = _synthetic(sizes, n, k, 5)
+    m = sum(sizes)
+    tmap = torch.full((tg.max_tiles(m, len(sizes), n), 9), -1, dtype=torch.int32, device=DEV)
+    out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
+                              tile_map=tmap)
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    assert_parity(got, oracle_c(ac, asc, bc, bsc, sizes), label="G=4096")
+    tm = tmap.cpu().numpy()
+    tm = sorted(tuple(int(x) for x in r) for r in tm[tm[:, 0] >= 0])
+    assert tm == sorted(oplan.kernel_tile_map(sizes, n, "pair_n256", num_pairs=_pairs(sizes, n)))
+
+
+def test_too_many_groups_is_unsupported_not_wrong():
+    sizes = (5,) + (0,) * 19999
+    ac, asc, bc, bsc = _synthetic(sizes[:1], 128, 128, 1)
+    bc = np.broadcast_to(bc, (len(sizes),) + bc.shape[1:]).copy()
+    bsc = np.broadcast_to(bsc, (len(sizes),) + bsc.shape[1:]).copy()
+    with pytest.raises(tg.Unsupported):
+        tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)))
