@@ -23,7 +23,7 @@
 
 namespace tagg {
 
-constexpr int kRouteChunk = 1024;  // rows per route chunk (one warp ranks a chunk in order)
+constexpr int kRouteChunk = 256;  // rows per route chunk (one warp ranks a chunk in order)
 constexpr int kMaxExperts = 1024;
 
 __global__ void __launch_bounds__(256) route_hist_kernel(const int32_t* __restrict__ eid, int64_t R, int E,
@@ -57,25 +57,34 @@ __global__ void __launch_bounds__(256) route_scan_kernel(int32_t* __restrict__ c
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (e >= E) return;
   int32_t* col = counts + static_cast<int64_t>(e) * nchunks;
-  const int cpl = (nchunks + 31) / 32;
-  const int c0 = min(nchunks, lane * cpl), c1 = min(nchunks, c0 + cpl);
-  int sum = 0;
-#pragma unroll 8
-  for (int c = c0; c < c1; ++c) sum += col[c];
-  int incl = sum;
+  // segments of 1024 chunks: lane l holds chunks [32 l, 32 l + 32) of the segment in
+  // registers (all loads in flight at once), one warp scan, then the prefix goes back
+  constexpr int kPer = 32;
+  int carry = 0;
+  for (int seg = 0; seg < nchunks; seg += 32 * kPer) {
+    const int c0 = seg + lane * kPer;
+    int v[kPer];
+    int sum = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
+    for (int i = 0; i < kPer; ++i) {
+      v[i] = c0 + i < nchunks ? col[c0 + i] : 0;
+      sum += v[i];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int run = carry + incl - sum;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      if (c0 + i < nchunks) col[c0 + i] = run;
+      run += v[i];
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
   }
-  int run = incl - sum;
-#pragma unroll 8
-  for (int c = c0; c < c1; ++c) {
-    const int v = col[c];
-    col[c] = run;
-    run += v;
-  }
-  if (lane == 31) group_sizes[e] = incl;
+  if (lane == 0) group_sizes[e] = carry;
 }
 
 // One warp per chunk, 32 rows at a time in order: lanes with the same expert find
@@ -108,10 +117,19 @@ __global__ void __launch_bounds__(32) route_rank_kernel(const int32_t* __restric
   }
   __syncwarp();
   const int64_t r0 = static_cast<int64_t>(c) * kRouteChunk;
-  for (int s = 0; s < kRouteChunk; s += 32) {
-    const int64_t r = r0 + s + lane;
+  // every id of the chunk is loaded up front (8 loads in flight per lane), then ranked in order
+  constexpr int kSteps = kRouteChunk / 32;
+  int ids[kSteps];
+#pragma unroll
+  for (int i = 0; i < kSteps; ++i) {
+    const int64_t r = r0 + 32 * i + lane;
+    ids[i] = r < R ? eid[r] : -1;
+  }
+#pragma unroll
+  for (int i = 0; i < kSteps; ++i) {
+    const int64_t r = r0 + 32 * i + lane;
     const bool ok = r < R;
-    int e = ok ? eid[r] : -1;
+    int e = ids[i];
     if (e >= E) e = -1;  // invalid ids were flagged by route_hist_kernel
     const uint32_t same = __match_any_sync(0xffffffffu, e);
     const int rank = __popc(same & ((1u << lane) - 1u));
@@ -124,7 +142,6 @@ __global__ void __launch_bounds__(32) route_rank_kernel(const int32_t* __restric
       if (lane == leader) run[e] += __popc(same);
     }
     __syncwarp();
-    if (s + 32 >= kRouteChunk || r0 + s + 32 >= R) break;
   }
 }
 
@@ -152,27 +169,46 @@ __global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __re
   // A warp covers 4 tiles per step: lane l holds 16 consecutive columns of tile
   // 4 step + l / 8 (8 lanes per 128-column tile): 32-B loads, 16-B code stores.
   const int sub = lane >> 3, part = lane & 7;
+  // Raw 16-byte loads of the next step are issued before the current step is quantized
+  // and scattered (2 steps of loads in flight per warp: the kernel is bound by memory
+  // parallelism, not bandwidth, at one step).
+  constexpr int kRaw = kBf16 ? 2 : 4;
+  auto full_at = [&](int tile0) { return vec && (tile0 + sub) * 128 + 16 * part + 15 < K; };
+  auto load_raw = [&](int tile0, uint4 (&r)[kRaw]) {
+    const int c0 = (tile0 + sub) * 128 + 16 * part;
+    const uint4* src = kBf16 ? reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + t * ldx + c0)
+                             : reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(x) + t * ldx + c0);
+#pragma unroll
+    for (int j = 0; j < kRaw; ++j) r[j] = __ldcs(src + j);  // read once: stream past L2
+  };
+  uint4 nxt[kRaw];
+  bool nxt_full = full_at(0);
+  if (nxt_full) load_raw(0, nxt);
   for (int tile0 = 0; tile0 < kb; tile0 += 4) {
     const int tile = tile0 + sub;
     const int c0 = tile * 128 + 16 * part;
+    const bool full16 = nxt_full;
+    uint4 cur[kRaw];
+#pragma unroll
+    for (int j = 0; j < kRaw; ++j) cur[j] = nxt[j];
+    nxt_full = tile0 + 4 < kb && full_at(tile0 + 4);
+    if (nxt_full) load_raw(tile0 + 4, nxt);
     float v[16];
-    const bool full16 = vec && c0 + 15 < K;
     if (full16) {
       if constexpr (kBf16) {
-        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + t * ldx + c0);
-        const uint4 r0 = src[0], r1 = src[1];
-        const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        const uint32_t w[8] = {cur[0].x, cur[0].y, cur[0].z, cur[0].w, cur[1].x, cur[1].y, cur[1].z, cur[1].w};
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           v[2 * j] = __uint_as_float(w[j] << 16);
           v[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
         }
       } else {
-        const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + t * ldx + c0);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float4 f = src[j];
-          v[4 * j] = f.x; v[4 * j + 1] = f.y; v[4 * j + 2] = f.z; v[4 * j + 3] = f.w;
+          v[4 * j] = __uint_as_float(cur[j].x);
+          v[4 * j + 1] = __uint_as_float(cur[j].y);
+          v[4 * j + 2] = __uint_as_float(cur[j].z);
+          v[4 * j + 3] = __uint_as_float(cur[j].w);
         }
       }
     } else {
@@ -331,7 +367,7 @@ extern "C" int tagg_route_plan(const int32_t* expert_ids, int64_t rows, int num_
                                                                                            : TAGG_ERR_CUDA;
   }
   route_hist_kernel<<<nchunks, 256, 0, st>>>(expert_ids, rows, num_experts, workspace, err);
-  route_scan_kernel<<<(num_experts + 7) / 8, 256, 0, st>>>(workspace, nchunks, num_experts, group_sizes);
+  route_scan_kernel<<<num_experts, 32, 0, st>>>(workspace, nchunks, num_experts, group_sizes);
   route_rank_kernel<<<nchunks, 32, 0, st>>>(expert_ids, rows, num_experts, workspace, group_sizes, dest_rows);
   return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
 }
