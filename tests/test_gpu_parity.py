@@ -339,3 +339,31 @@ def test_too_many_groups_is_unsupported_not_wrong():
     bsc = np.broadcast_to(bsc, (len(sizes),) + bsc.shape[1:]).copy()
     with pytest.raises(tg.Unsupported):
         tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)))
+
+
+def test_host_batches_overlapped_copies_match_direct_calls():
+    """hostpipe.run_host_batches (H2D / GEMM / D2H on three streams, slots reused) writes each
+    batch's C rows to its host tensor exactly as direct calls do."""
+    from paper_2508_16584_b200.hostpipe import HostBatch, run_host_batches
+
+    n, k, G = 256, 384, 3
+    batches, wants = [], []
+    _, _, bc, bsc = _synthetic((1, 1, 1), n, k, 77)
+    b, sb = _dev(bc), _dev(bsc)
+    for i in range(5):
+        sizes = (37 * i + 1, 0 if i % 2 else 130, 64 + i)
+        ac, asc, _, _ = _synthetic(sizes, n, k, i)
+        gs = torch.tensor(sizes, dtype=torch.int32)
+        on_host = i != 3  # one batch with device-resident inputs
+        a = torch.from_numpy(ac).pin_memory() if on_host else _dev(ac)
+        sa = torch.from_numpy(asc).pin_memory() if on_host else _dev(asc)
+        out = torch.full((sum(sizes) + 5, n), 0x7BCD, dtype=torch.int16).pin_memory()
+        batches.append(HostBatch(a, sa, gs.pin_memory(), out))
+        want = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), b, sb, gs.to(DEV))
+        wants.append(want[:sum(sizes)].view(torch.int16).cpu())
+    done = run_host_batches(batches, b, sb, depth=2)
+    done.synchronize()
+    for bt, want in zip(batches, wants):
+        m = want.shape[0]
+        assert torch.equal(bt.out[:m], want)
+        assert bool((bt.out[m:] == 0x7BCD).all())  # rows past sum(M_g) untouched
