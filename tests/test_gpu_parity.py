@@ -367,3 +367,25 @@ def test_host_batches_overlapped_copies_match_direct_calls():
         m = want.shape[0]
         assert torch.equal(bt.out[:m], want)
         assert bool((bt.out[m:] == 0x7BCD).all())  # rows past sum(M_g) untouched
+
+
+def test_acceptance_random_configs_bitwise_vs_padded_and_oracle():
+    """The reference's acceptance 06 (test_acceptance.py:180-201) on the GPU: 100 random
+    configs (1/4/8 groups of 0..512 rows, N and K in {128, 192, 256, 384}, the reference's
+    operand recipe).  The padding-free path equals the padded baseline bit for bit, and both
+    match the oracle within helpers.REL_TOL."""
+    rng = np.random.Generator(np.random.PCG64(2024))
+    dims = (128, 192, 256, 384)
+    for i in range(100):
+        groups = int(rng.choice((1, 4, 8)))
+        sizes = tuple(int(x) for x in rng.integers(0, 513, size=groups))
+        n, k = int(rng.choice(dims)), int(rng.choice(dims))
+        m = sum(sizes)
+        ac, asc, bc, bsc = ofp8.random_operands(m, n, k, i)
+        cfg = tg.ProblemConfig(n=n, k=k, group_sizes=sizes)
+        ops = tg.GroupedOperands(ac, asc, bc, bsc)
+        got = tg.run_adaptive(cfg, ops).c_bits
+        want = tg.run_padded_baseline(cfg, ops)
+        assert tg.verify_bitwise(got, want).equal, (i, sizes, n, k)
+        if m:
+            assert_parity(got, oracle_c(ac, asc, bc, bsc, sizes), label=f"config {i}")
