@@ -58,6 +58,14 @@ extern "C" {
 #define TAGG_FLAG_TILE_N128 8u       /* CTA-pair tile 256x128 (more, smaller tiles: fewer idle SMs
                                         in the last wave of small problems) */
 #define TAGG_FLAG_TILE_N256 16u      /* CTA-pair tile 256x256 (the default) */
+#define TAGG_FLAG_SERIAL 32u         /* no programmatic dependent launch.  By default a grouped GEMM
+                                        is launched with PDL: when the previous kernel in the stream
+                                        is a grouped GEMM, this one's CTAs start on the SMs that grid
+                                        releases and run their main loop; they wait for its completion
+                                        (griddepcontrol.wait) only before their first global store.
+                                        So its inputs must not be written by the grouped GEMM launched
+                                        right before it (any other kernel in between restores full
+                                        ordering: it triggers only at completion). */
 /* Cap the persistent grid at n SMs (flags bits 16-27; 0 = every SM).  An overlapped
    expert-parallel exchange leaves the rest to the NCCL kernels that run beside the GEMM. */
 #define TAGG_SM_LIMIT_SHIFT 16

@@ -293,6 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   tc_fence_before();
   if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
+  // The next grouped GEMM in the stream (PDL launch) may start on SMs this grid releases;
+  // it only waits for this grid before its first global store (see griddep_wait below).
+  griddep_launch_dependents();
   // Values needed after the setmaxnreg split are re-read inside each role (ld.shared is
   // cheap); keeping them live across it makes ptxas spill them into the hot loops.
   const int kbc = p.kb_count;
@@ -455,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
     uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0, tiles_done = 0;
+    bool prev_grid_done = false;
 #ifdef TAGG_TRACE
     const bool tr_a = p.trace != nullptr && pw == 0 && lane == 0;
     const bool tr_b = p.trace != nullptr && pw == 4 && lane == 0;
@@ -532,6 +536,10 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           fence_proxy_async_smem();
         }
         named_bar_sync(1, 32 * kNumPromoWarps);
+        if (ptid == 0 && T.valid > 0 && !prev_grid_done) {
+          griddep_wait();  // WAW on C / tile_map with the previous grid: store only after it completed
+          prev_grid_done = true;
+        }
         if (ptid == 0 && T.valid > 0) {
           for (int ch = 0; ch < 4; ++ch) {
             const int col = T.n0 + 64 * ch;
@@ -657,6 +665,10 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           fence_proxy_async_smem();
         }
         named_bar_sync(1, 32 * kNumPromoWarps);
+        if (ptid == 0 && T.valid > 0 && !prev_grid_done) {
+          griddep_wait();  // WAW on C / tile_map with the previous grid: store only after it completed
+          prev_grid_done = true;
+        }
         if (ptid == 0 && T.valid > 0) {
           const int nchunks = (kBN == 256 && passes == 1) ? 4 : 2;
           for (int ch = 0; ch < nchunks; ++ch) {
@@ -846,7 +858,7 @@ static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_a
 }
 
 template <int kCG, int kBN, bool kExact, bool kSwizzleC>
-static cudaError_t launch(const Params& p, uint32_t smem_bytes, int grid, cudaStream_t stream) {
+static cudaError_t launch(const Params& p, uint32_t smem_bytes, int grid, cudaStream_t stream, bool pdl) {
   auto kern = tagg_gemm_kernel<kCG, kBN, kExact, kSwizzleC>;
   static bool configured = false;
   if (!configured) {
@@ -859,23 +871,26 @@ static cudaError_t launch(const Params& p, uint32_t smem_bytes, int grid, cudaSt
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1] = {};
+  cudaLaunchAttribute attr[2] = {};
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = kCG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 template <int kCG, int kBN>
-static cudaError_t launch_cfg(const Params& p, uint32_t smem_bytes, int grid, cudaStream_t st, bool exact, bool swz) {
+static cudaError_t launch_cfg(const Params& p, uint32_t smem_bytes, int grid, cudaStream_t st, bool exact, bool swz,
+                              bool pdl) {
   if (exact)
-    return swz ? launch<kCG, kBN, true, true>(p, smem_bytes, grid, st)
-               : launch<kCG, kBN, true, false>(p, smem_bytes, grid, st);
-  return swz ? launch<kCG, kBN, false, true>(p, smem_bytes, grid, st)
-             : launch<kCG, kBN, false, false>(p, smem_bytes, grid, st);
+    return swz ? launch<kCG, kBN, true, true>(p, smem_bytes, grid, st, pdl)
+               : launch<kCG, kBN, true, false>(p, smem_bytes, grid, st, pdl);
+  return swz ? launch<kCG, kBN, false, true>(p, smem_bytes, grid, st, pdl)
+             : launch<kCG, kBN, false, false>(p, smem_bytes, grid, st, pdl);
 }
 
 
@@ -1054,9 +1069,12 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool exact = (flags & TAGG_FLAG_EXACT_PROMOTION) != 0;
   cudaError_t e;
-  if (cg == 1) e = launch_cfg<1, 128>(p, smem_bytes, grid, st, exact, swz);
-  else if (bn == 128) e = launch_cfg<2, 128>(p, smem_bytes, grid, st, exact, swz);
-  else e = launch_cfg<2, 256>(p, smem_bytes, grid, st, exact, swz);
+  // PDL: this launch may start while the previous grid in the stream drains (it stores only
+  // after that grid completed); TAGG_FLAG_SERIAL restores plain stream order
+  const bool pdl = (flags & TAGG_FLAG_SERIAL) == 0;
+  if (cg == 1) e = launch_cfg<1, 128>(p, smem_bytes, grid, st, exact, swz, pdl);
+  else if (bn == 128) e = launch_cfg<2, 128>(p, smem_bytes, grid, st, exact, swz, pdl);
+  else e = launch_cfg<2, 256>(p, smem_bytes, grid, st, exact, swz, pdl);
   if (e != cudaSuccess) {
     std::fprintf(stderr, "tagg_grouped_gemm_fp8: launch failed: %s\n", cudaGetErrorString(e));
     return TAGG_ERR_CUDA;

@@ -32,6 +32,7 @@ FLAG_PLAIN_C_STAGING = 2
 FLAG_SINGLE_CTA = 4
 FLAG_TILE_N128 = 8
 FLAG_TILE_N256 = 16
+FLAG_SERIAL = 32  # no programmatic dependent launch (include/tagg.h TAGG_FLAG_SERIAL)
 SM_LIMIT_SHIFT = 16  # TAGG_SM_LIMIT(n): cap the persistent grid at n SMs (include/tagg.h)
 TILES = {None: 0, "auto": 0, "1cta": FLAG_SINGLE_CTA, "pair_n128": FLAG_TILE_N128, "pair_n256": FLAG_TILE_N256}
 TILE_MAP_FIELDS = 9
@@ -175,7 +176,7 @@ def _ptr(t):
 
 def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", out=None, c_row_offsets=None,
                      tile_map=None, exact_promotion=False, plain_staging=False, single_cta=False, tile=None,
-                     stream=None, max_sms=None):
+                     stream=None, max_sms=None, pdl=True):
     """Padding-free FP8 grouped GEMM on device tensors (no host sync).
 
     a [m_alloc,K] uint8 / float8_e4m3fn; a_scales [m_alloc,ceil(K/128)] f32;
@@ -235,7 +236,7 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
     if c_row_offsets is not None and (c_row_offsets.dtype != torch.int64 or not c_row_offsets.is_cuda):
         raise ShapeMismatch("c_row_offsets must be an int64 CUDA tensor")
     flags = ((FLAG_EXACT_PROMOTION if exact_promotion else 0) | (FLAG_PLAIN_C_STAGING if plain_staging else 0)
-             | (FLAG_SINGLE_CTA if single_cta else 0) | TILES[tile])
+             | (FLAG_SINGLE_CTA if single_cta else 0) | TILES[tile] | (0 if pdl else FLAG_SERIAL))
     if max_sms:
         if not 0 < int(max_sms) < 4096:
             raise ConfigError(f"max_sms must be in [1, 4095], got {max_sms}")

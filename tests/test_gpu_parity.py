@@ -389,3 +389,28 @@ def test_acceptance_random_configs_bitwise_vs_padded_and_oracle():
         assert tg.verify_bitwise(got, want).equal, (i, sizes, n, k)
         if m:
             assert_parity(got, oracle_c(ac, asc, bc, bsc, sizes), label=f"config {i}")
+
+
+@pytest.mark.parametrize("pdl", [True, False])
+def test_back_to_back_launches_into_one_buffer_keep_stream_order(pdl):
+    """Programmatic dependent launch: a grouped GEMM may start while the previous one drains,
+    but stores only after it completed.  A long GEMM then a short one into the same output,
+    with no sync between: the short one's rows hold its result, the rest the long one's."""
+    n, k = 512, 1024
+    big = (4000, 3000, 2500)
+    small = (300, 0, 17)
+    ab, asb, bcb, bsb = _synthetic(big, n, k, 1)
+    as_, ass, bcs, bss = _synthetic(small, n, k, 2)
+    want_big = tg.grouped_gemm_fp8(_dev(ab), _dev(asb), _dev(bcb), _dev(bsb), _dev(np.array(big, np.int32)))
+    want_small = tg.grouped_gemm_fp8(_dev(as_), _dev(ass), _dev(bcs), _dev(bss), _dev(np.array(small, np.int32)))
+    ms = sum(small)
+    args_big = (_dev(ab), _dev(asb), _dev(bcb), _dev(bsb), _dev(np.array(big, np.int32)))
+    args_small = (_dev(as_), _dev(ass), _dev(bcs), _dev(bss), _dev(np.array(small, np.int32)))
+    out = torch.empty((sum(big), n), dtype=torch.bfloat16, device=DEV)
+    torch.cuda.synchronize()
+    for _ in range(20):
+        tg.grouped_gemm_fp8(*args_big, out=out, pdl=pdl)
+        tg.grouped_gemm_fp8(*args_small, out=out, pdl=pdl)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:ms].view(torch.int16), want_small[:ms].view(torch.int16))
+    assert torch.equal(out[ms:].view(torch.int16), want_big[ms:].view(torch.int16))
