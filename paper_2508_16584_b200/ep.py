@@ -68,13 +68,11 @@ def dispatch(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_ids: torch.Te
     for this rank's experts and meta.group_sizes holds the device group sizes.
     """
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     if num_experts % world:
         raise ValueError(f"{num_experts} experts do not split over {world} ranks")
     epr = num_experts // world
     if a_codes.dtype == torch.float8_e4m3fn:
         a_codes = a_codes.view(torch.uint8)
-    dev = a_codes.device
     order = torch.argsort(expert_ids.to(torch.int64), stable=True)
     a_sorted = a_codes.index_select(0, order)
     sa_sorted = a_scales.index_select(0, order)
@@ -106,7 +104,6 @@ def dispatch_tokens(x: torch.Tensor, expert_ids: torch.Tensor, num_experts: int,
 def _exchange(a_sorted, sa_sorted, counts, order, epr, group, inv_order=None):
     """All-to-all of expert-sorted local rows; regroup received rows to expert-contiguous."""
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     dev = a_sorted.device
     a_codes, a_scales = a_sorted, sa_sorted
     recv_counts = torch.empty_like(counts)                          # [P * epr] from each source
@@ -135,7 +132,6 @@ def _exchange(a_sorted, sa_sorted, counts, order, epr, group, inv_order=None):
     sa_local = sa_recv.index_select(0, to_grouped)
     meta = DispatchMeta(order, send_splits, recv_splits, to_grouped, group_sizes.to(dev), epr,
                         from_grouped=_inverse(to_grouped), inv_order=_inverse(order) if inv_order is None else inv_order)
-    del rank
     return a_local, sa_local, meta
 
 
