@@ -1,0 +1,40 @@
+"""Small invocations of every product kernel, for compute-sanitizer (memcheck / racecheck /
+synccheck): python tools/sanitize.py"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+import paper_2508_16584_b200 as tg  # noqa: E402
+from oracle import fp8 as ofp8  # noqa: E402
+
+dev = torch.device("cuda", 0)
+sizes = (1, 67, 0, 128, 255, 300)
+n, k = 384, 640
+m = sum(sizes)
+ac, asc, _, _ = ofp8.random_operands(m, 64, k, 3)
+bs = [ofp8.random_operands(1, n, k, 10 + g) for g in range(len(sizes))]
+bc = np.stack([b[2] for b in bs])
+bsc = np.stack([b[3] for b in bs])
+a, sa = torch.from_numpy(ac).to(dev), torch.from_numpy(asc).to(dev)
+b, sb = torch.from_numpy(bc).to(dev), torch.from_numpy(bsc).to(dev)
+gs = torch.tensor(sizes, dtype=torch.int32, device=dev)
+for tile in ("pair_n256", "pair_n128", "1cta"):
+    for exact in (False, True):
+        tg.grouped_gemm_fp8(a, sa, b, sb, gs, tile=tile, exact_promotion=exact)
+# exact-size output: any store past sum(M_g) would be out of bounds
+out = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
+tg.grouped_gemm_fp8(a[:m].contiguous(), sa[:m].contiguous(), b, sb, gs, out=out)
+ws = tg.PaddedWorkspace(m, len(sizes), k, n, dev)
+tg.padded_grouped_gemm_fp8(a, sa, b, sb, gs, ws)
+x = torch.randn((100, k), device=dev)
+eids = torch.randint(0, 6, (100, 4), device=dev, dtype=torch.int32)
+d = tg.quantize_dispatch(x, eids, 6)
+tg.quantize_blocks(torch.randn((2, 256, 384), device=dev))
+xc, xs = tg.quantize_col_blocks(torch.randn((m, 256), device=dev), gs)
+dyc, dys = tg.quantize_col_blocks(torch.randn((m, 128), device=dev), gs)
+tg.wgrad_fp8(xc, xs, dyc, dys, gs)
+torch.cuda.synchronize()
+print("sanitize workload done")
