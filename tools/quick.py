@@ -31,6 +31,12 @@ shapes = [
     ("ds_gateup", [tuple(int(x) for x in deepseek_gateup_sizes(0)[1])], 4096, 7168, 32, "kn"),
     ("qwen_dgrad_gu", None, 4096, 3072, 128, "nk"),
     ("ds_down", [tuple(int(x) for x in deepseek_gateup_sizes(seed=1)[0])], 7168, 2048, 256, "kn"),
+    ("qwen_fwd_gu", [tuple(int(x) for x in deepseek_gateup_sizes(seed=2, experts=128, local=128)[0])], 3072, 4096, 128,
+     "kn"),
+    ("qwen_fwd_down", [tuple(int(x) for x in deepseek_gateup_sizes(seed=2, experts=128, local=128)[0])], 4096, 1536,
+     128, "kn"),
+    ("qwen_dgrad_down", [tuple(int(x) for x in deepseek_gateup_sizes(seed=2, experts=128, local=128)[0])], 1536, 4096,
+     128, "nk"),
 ]
 only = [a for a in args[1:]] if len(args) > 1 else None
 shapes = [s for s in shapes if only is None or s[0] in only]
