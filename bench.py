@@ -526,6 +526,7 @@ def run_extra(torch, tg, dev, rank, fp8_peak, exact):
         torch.cuda.empty_cache()
     out["quantize_dispatch_dsv3"] = run_quantize_dispatch(torch, tg, dev)
     out["wgrad_dsv3_gateup"] = run_wgrad(torch, tg, dev, fp8_peak)
+    out["moe_ffn_dsv3_1gpu"] = run_moe_ffn(torch, tg, dev, fp8_peak)
     return out
 
 
@@ -581,6 +582,65 @@ def run_quantize_dispatch(torch, tg, dev, tokens=32768, k=7168, topk=8, experts=
     return {"tokens": tokens, "K": k, "topk": topk, "experts": experts, "ms": ms,
             "algorithmic_bytes": nbytes, "gbs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / peak,
             "hbm_peak_gbs": peak, "note": "route plan (3 launches) + quantize/scatter (1 launch), x resident"}
+
+
+def run_moe_ffn(torch, tg, dev, fp8_peak, tokens=32768, topk=8, experts=256, hidden=7168, inter=2048, iters=5,
+                warmup=2):
+    """The whole padding-free MoE FFN forward at DeepSeek-V3 scale on one GPU (all 256
+    experts): quantize + dispatch -> GEMM gate|up -> SwiGLU + quantize -> GEMM down ->
+    top-k combine.  Per-step device times from events on the one stream."""
+    from paper_2508_16584_b200 import moe, quant
+
+    g = torch.Generator(device=dev).manual_seed(11)
+    x = torch.randn((tokens, hidden), device=dev, generator=g).to(torch.bfloat16)
+    logits = torch.randn((tokens, experts), device=dev, generator=g)
+    top = torch.topk(logits, topk, dim=1)
+    eids = top.indices.to(torch.int32)
+    wts = torch.softmax(top.values, dim=1)
+    w = moe.ExpertWeights(_codes(torch, (experts, hidden, 2 * inter), g, dev),
+                          _scales(torch, (experts, hidden // 128, 2 * inter // 128), g, dev),
+                          _codes(torch, (experts, inter, hidden), g, dev),
+                          _scales(torch, (experts, inter // 128, hidden // 128), g, dev))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    names = ("quantize_dispatch", "gemm_gate_up", "swiglu_quantize", "gemm_down", "combine")
+    acc = [0.0] * 5
+
+    def step(timed):
+        if timed:
+            ev[0].record()
+        d = quant.quantize_dispatch(x, eids, experts)
+        if timed:
+            ev[1].record()
+        h = tg.grouped_gemm_fp8(d.a_codes, d.a_scales, w.w_gate_up, w.s_gate_up, d.group_sizes)
+        if timed:
+            ev[2].record()
+        a2, s2 = moe.swiglu_quantize(h, d.group_sizes)
+        if timed:
+            ev[3].record()
+        c = tg.grouped_gemm_fp8(a2, s2, w.w_down, w.s_down, d.group_sizes)
+        if timed:
+            ev[4].record()
+        y = moe.combine(c, d.dest_rows, wts)
+        if timed:
+            ev[5].record()
+        return y
+
+    for _ in range(warmup):
+        step(False)
+    torch.cuda.synchronize()
+    for _ in range(iters):
+        step(True)
+        torch.cuda.synchronize()
+        for i in range(5):
+            acc[i] += ev[i].elapsed_time(ev[i + 1])
+    ms = [a / iters for a in acc]
+    rows = tokens * topk
+    flops = 2.0 * rows * hidden * 2 * inter + 2.0 * rows * inter * hidden
+    total = sum(ms)
+    return {"tokens": tokens, "topk": topk, "experts": experts, "hidden": hidden, "intermediate": inter,
+            "ms": total, "tflops": flops / (total * 1e-3) / 1e12, "fp8_peak_frac": flops / (total * 1e-3) / 1e12 / fp8_peak,
+            "breakdown_ms": dict(zip(names, ms)),
+            "note": "all intermediates padding-free (no pad rows, no permutation between the GEMMs)"}
 
 
 def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, warmup=2):

@@ -220,6 +220,28 @@ const char* tagg_error_string(int code);
 void tagg_debug_trace(void* buf);
 int tagg_version(void);
 
+/* ---- MoE FFN steps around the GEMM (csrc/tagg_moe.cu) ---- */
+/*
+ * SwiGLU + 1x128 quantize of the gate|up GEMM output, in place in the padding-free layout:
+ *   h            bf16 [m_alloc, >= 2I], row pitch ldh elements: gate = columns [0, I),
+ *                up = columns [I, 2I)
+ *   group_sizes  DEVICE int32 [G]: only rows [0, sum M_g) are read and written
+ *   a / sa       the down GEMM's A: e4m3 codes [m_alloc, I] (pitch lda bytes) and fp32 scales
+ *                [m_alloc, ceil(I/128)], from v = fl(silu(gate) * up) with the fp8.py:132-151 recipe
+ *   err_flag     DEVICE int32, |= 2 on a non-finite v
+ * ldh*2, I*2, lda and both bases must be multiples of 16 bytes.
+ */
+int tagg_swiglu_quantize(const void* h, int64_t ldh, const int32_t* group_sizes, int G, int64_t m_alloc, int I,
+                         void* a, int64_t lda, float* sa, int32_t* err_flag, void* stream);
+/*
+ * Top-k combine of the down GEMM output: out[t, :] = bf16( sum_{k < topk} fl(w[t,k] * c[dest[t*topk+k], :]) ),
+ * accumulated in fp32 in k order with separate roundings (no FMA).  dest = the dispatch plan's
+ * dest_rows (tagg_route_plan); c bf16 [rows, N] (pitch ldc), out bf16 [tokens, N] (pitch ldo),
+ * N % 8 == 0, topk <= 8, 16-byte aligned bases and pitches.
+ */
+int tagg_combine(const void* c, int64_t ldc, const int32_t* dest_rows, const float* weights, int64_t tokens, int topk,
+                 int N, void* out, int64_t ldo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,7 @@ from .quant import (  # noqa: F401
 )
 from .wgrad import quantize_col_blocks, wgrad_fp8  # noqa: F401
 from . import tensorio  # noqa: F401
+from . import moe  # noqa: F401
 from .hostpipe import HostBatch, run_host_batches  # noqa: F401
 from .tensorio import load_tensor, read_fixture, read_tensor, save_tensor, write_fixture, write_tensor  # noqa: F401
 from .planning import (  # noqa: F401

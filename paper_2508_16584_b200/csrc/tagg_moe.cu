@@ -1,0 +1,190 @@
+// tagg_moe.cu -- the two HBM-bound steps that close an MoE FFN around the padding-free GEMM:
+//
+//   K7 swiglu_quantize_kernel: gate|up GEMM output (grouped rows, bf16 [M, 2I]) ->
+//      h = silu(gate) * up in fp32 (fast exp / division, a few ulp) -> the 1x128 FP8 recipe
+//      of fp8.py:132-151 (amax -> s = fl(amax/448) -> e4m3(h * fl(1/s)), RNE, saturating;
+//      the reciprocal in place of the recipe's division) -> the down GEMM's A and S_A, in the
+//      same padding-free grouped rows (no permutation, no pad rows).  Rows past sum(M_g)
+//      are not touched (the group sizes stay on the device).
+//   K8 combine_kernel: down GEMM output (grouped rows, bf16 [R, N]) -> per token
+//      out[t] = bf16( sum_k fl(w[t,k] * c[dest[t*topk+k]]) ) accumulated in fp32 in k order,
+//      separately rounded (no FMA), so a CPU restatement reproduces it bit for bit.
+//
+// Both are memory-bound byte/float work: 16-byte vector accesses, one warp per row (K7) or
+// one CTA per token (K8), no tensor cores.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tagg.h"
+
+namespace tagg {
+namespace moe {
+
+__device__ __forceinline__ uint16_t e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// silu(g) * u in fp32: g / (1 + e^-g) with the fast ex2-based exp and an approximate
+// division (a few ulp; the result is quantized to 3 mantissa bits next).  The accurate
+// expf + IEEE division made the kernel compute-bound at 6x its HBM time.
+__device__ __forceinline__ float swiglu(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
+
+// One warp per row; lane l holds 16 consecutive columns of tile 4 step + l / 8.
+__global__ void __launch_bounds__(256) swiglu_quantize_kernel(const uint16_t* __restrict__ h, int64_t ldh,
+                                                              const int32_t* __restrict__ group_sizes, int G,
+                                                              int64_t m_alloc, int I, uint8_t* __restrict__ a,
+                                                              int64_t lda, float* __restrict__ sa,
+                                                              int32_t* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  // rows in use = sum of the device group sizes (every warp reduces them; G is small)
+  int64_t total = 0;
+  for (int g = lane; g < G; g += 32) total += max(0, group_sizes[g]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  total = min(total, m_alloc);
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= total) return;
+  const int kb = (I + 127) / 128;
+  const int sub = lane >> 3, part = lane & 7;
+  const uint16_t* hg = h + row * ldh;  // gate: columns [0, I)
+  const uint16_t* hu = hg + I;         // up:   columns [I, 2I)
+  bool bad = false;
+  for (int tile0 = 0; tile0 < kb; tile0 += 4) {
+    const int tile = tile0 + sub;
+    const int c0 = tile * 128 + 16 * part;
+    float v[16];
+    if (tile < kb && c0 + 15 < I) {
+      const uint4* pg = reinterpret_cast<const uint4*>(hg + c0);
+      const uint4* pu = reinterpret_cast<const uint4*>(hu + c0);
+      const uint4 g0 = pg[0], g1 = pg[1], u0 = pu[0], u1 = pu[1];
+      const uint32_t gw[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const uint32_t uw[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[2 * j] = swiglu(bf16_lo(gw[j]), bf16_lo(uw[j]));
+        v[2 * j + 1] = swiglu(bf16_hi(gw[j]), bf16_hi(uw[j]));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        v[j] = (tile < kb && c0 + j < I) ? swiglu(__uint_as_float(static_cast<uint32_t>(hg[c0 + j]) << 16),
+                                                  __uint_as_float(static_cast<uint32_t>(hu[c0 + j]) << 16))
+                                         : 0.0f;
+    }
+    float amax = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float m = fabsf(v[j]);
+      bad |= !(m <= 3.402823466e38f);
+      amax = fmaxf(amax, m);
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+    // v * (1/s) instead of the recipe's IEEE v / s: v is itself a few ulp off (fast exp),
+    // and the IEEE division sequence made this kernel issue-bound (79 instructions per
+    // element); the two differ by at most one fp32 ulp before the 3-bit rounding
+    const float inv = __frcp_rn(s);
+    uint32_t word[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint16_t lo = e4m3x2(__fmul_rn(v[4 * j], inv), __fmul_rn(v[4 * j + 1], inv));
+      const uint16_t hi = e4m3x2(__fmul_rn(v[4 * j + 2], inv), __fmul_rn(v[4 * j + 3], inv));
+      word[j] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    }
+    if (tile < kb) {
+      uint8_t* dst = a + row * lda + c0;
+      if (c0 + 15 < I) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(word[0], word[1], word[2], word[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < I) dst[j] = static_cast<uint8_t>(word[j >> 2] >> (8 * (j & 3)));
+      }
+      if (part == 0) sa[row * kb + tile] = s;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 2);
+}
+
+// One CTA per token; thread i owns 8-column groups i, i + blockDim, ...
+__global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict__ c, int64_t ldc,
+                                                      const int32_t* __restrict__ dest,
+                                                      const float* __restrict__ w, int topk, int N,
+                                                      uint16_t* __restrict__ out, int64_t ldo) {
+  const int64_t t = blockIdx.x;
+  __shared__ int32_t rows[8];
+  __shared__ float ws[8];
+  if (threadIdx.x < topk) {
+    rows[threadIdx.x] = dest[t * topk + threadIdx.x];
+    ws[threadIdx.x] = w[t * topk + threadIdx.x];
+  }
+  __syncthreads();
+  for (int c8 = threadIdx.x; c8 * 8 < N; c8 += blockDim.x) {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    for (int k = 0; k < topk; ++k) {
+      const uint4 q = *reinterpret_cast<const uint4*>(c + static_cast<int64_t>(rows[k]) * ldc + 8 * c8);
+      const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+      const float wk = ws[k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[2 * j] = __fadd_rn(acc[2 * j], __fmul_rn(wk, bf16_lo(qw[j])));
+        acc[2 * j + 1] = __fadd_rn(acc[2 * j + 1], __fmul_rn(wk, bf16_hi(qw[j])));
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t r;
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(acc[2 * j + 1]), "f"(acc[2 * j]));
+      o[j] = r;
+    }
+    *reinterpret_cast<uint4*>(out + t * ldo + 8 * c8) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+}  // namespace moe
+}  // namespace tagg
+
+using namespace tagg;
+
+extern "C" int tagg_swiglu_quantize(const void* h, int64_t ldh, const int32_t* group_sizes, int G, int64_t m_alloc,
+                                    int I, void* a, int64_t lda, float* sa, int32_t* err_flag, void* stream) {
+  if (I < 1 || G < 1 || m_alloc < 0) return TAGG_ERR_CONFIG;
+  if (ldh < 2 * static_cast<int64_t>(I) || lda < I) return TAGG_ERR_SHAPE;
+  if (m_alloc == 0) return TAGG_OK;
+  if (!h || !group_sizes || !a || !sa || !err_flag) return TAGG_ERR_SHAPE;
+  // 16-byte vectors: row pitches and both halves' starts on 16-byte boundaries
+  if ((reinterpret_cast<uintptr_t>(h) % 16) || ((ldh * 2) % 16) || ((I * 2) % 16) ||
+      (reinterpret_cast<uintptr_t>(a) % 16) || (lda % 16))
+    return TAGG_ERR_ALIGNMENT;
+  const int warps = 8;
+  const int64_t blocks = (m_alloc + warps - 1) / warps;
+  if (blocks >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
+  moe::swiglu_quantize_kernel<<<static_cast<unsigned>(blocks), 32 * warps, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(h), ldh, group_sizes, G, m_alloc, I, static_cast<uint8_t*>(a), lda, sa, err_flag);
+  return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
+}
+
+extern "C" int tagg_combine(const void* c, int64_t ldc, const int32_t* dest_rows, const float* weights, int64_t tokens,
+                            int topk, int N, void* out, int64_t ldo, void* stream) {
+  if (tokens < 0 || topk < 1 || topk > 8 || N < 8 || N % 8) return TAGG_ERR_CONFIG;
+  if (ldc < N || ldo < N) return TAGG_ERR_SHAPE;
+  if (tokens == 0) return TAGG_OK;
+  if (!c || !dest_rows || !weights || !out) return TAGG_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(c) % 16) || ((ldc * 2) % 16) || (reinterpret_cast<uintptr_t>(out) % 16) ||
+      ((ldo * 2) % 16))
+    return TAGG_ERR_ALIGNMENT;
+  if (tokens >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
+  moe::combine_kernel<<<static_cast<unsigned>(tokens), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(c), ldc, dest_rows, weights, topk, N, static_cast<uint16_t*>(out), ldo);
+  return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
+}

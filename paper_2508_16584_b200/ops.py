@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import torch
 
-from . import engine, quant
+from . import engine, moe, quant
 
 _LIB = "tagg"
 
@@ -73,3 +73,28 @@ def wgrad_fp8(x_codes: torch.Tensor, x_scales: torch.Tensor, dy_codes: torch.Ten
 @wgrad_fp8.register_fake
 def _(x_codes, x_scales, dy_codes, dy_scales, group_sizes):
     return x_codes.new_empty((group_sizes.shape[0], x_codes.shape[1], dy_codes.shape[1]), dtype=torch.bfloat16)
+
+
+@torch.library.custom_op(f"{_LIB}::swiglu_quantize", mutates_args=(), device_types="cuda")
+def swiglu_quantize(h: torch.Tensor, group_sizes: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """gate|up bf16 rows -> the down GEMM's (codes, scales), padding-free (moe.py)."""
+    a, sa = moe.swiglu_quantize(h, group_sizes)
+    return a.contiguous(), sa
+
+
+@swiglu_quantize.register_fake
+def _(h, group_sizes):
+    i = h.shape[1] // 2
+    return h.new_empty((h.shape[0], i), dtype=torch.uint8), h.new_empty((h.shape[0], -(-i // 128)),
+                                                                       dtype=torch.float32)
+
+
+@torch.library.custom_op(f"{_LIB}::combine", mutates_args=(), device_types="cuda")
+def combine(c: torch.Tensor, dest_rows: torch.Tensor, weights: torch.Tensor) -> torch.Tensor:
+    """Top-k weighted combine of grouped rows back to tokens (moe.py)."""
+    return moe.combine(c, dest_rows, weights)
+
+
+@combine.register_fake
+def _(c, dest_rows, weights):
+    return c.new_empty((weights.shape[0], c.shape[1]), dtype=torch.bfloat16)

@@ -11,7 +11,8 @@ import paper_2508_16584_b200 as tg  # noqa: F401  (registers the ops)
 
 
 def test_ops_are_registered():
-    for name in ("grouped_gemm_fp8", "quantize_row_tiles", "quantize_dispatch", "wgrad_fp8"):
+    for name in ("grouped_gemm_fp8", "quantize_row_tiles", "quantize_dispatch", "wgrad_fp8", "swiglu_quantize",
+                 "combine"):
         assert hasattr(torch.ops.tagg, name)
 
 
@@ -39,6 +40,11 @@ def test_fake_kernels_infer_shapes():
         assert ac.shape == (40, 300) and asc.shape == (40, 3) and gsz.shape == (16,) and dest.shape == (40,)
         dw = torch.ops.tagg.wgrad_fp8(a[:, :256], sa, a[:, :128], sa, gs)
         assert dw.shape == (3, 256, 128) and dw.dtype == torch.bfloat16
+        hq, hs = torch.ops.tagg.swiglu_quantize(torch.empty((300, 512), dtype=torch.bfloat16, device="cuda"), gs)
+        assert hq.shape == (300, 256) and hs.shape == (300, 2)
+        y = torch.ops.tagg.combine(c, torch.empty((300,), dtype=torch.int32, device="cuda"),
+                                   torch.empty((75, 4), dtype=torch.float32, device="cuda"))
+        assert y.shape == (75, 256) and y.dtype == torch.bfloat16
 
 
 @pytest.mark.gpu

@@ -178,3 +178,23 @@ def test_kernel_tile_map_stores_exactly_the_reference_rows(sizes, pairs, raster)
         assert 1 <= valid and d <= valid < 2 * d
         assert ag + d <= off + sizes[g] and bg + d <= off + sizes[g]
         assert bg - ag == valid - d == bs
+
+
+def test_moe_oracle_combine_and_swiglu_against_float64():
+    """The MoE step oracles (oracle/moe.py) against float64 arithmetic."""
+    from oracle import moe as omoe
+
+    rng = np.random.default_rng(0)
+    c = omoe.bf16_rne(rng.standard_normal((40, 16)).astype(np.float32))
+    dest = rng.permutation(40).astype(np.int32)
+    w = rng.random((10, 4)).astype(np.float32)
+    got = ofp8.bf16_bits_to_f32(omoe.combine(c, dest, w)).astype(np.float64)
+    want = (w[:, :, None].astype(np.float64) * ofp8.bf16_bits_to_f32(c)[dest].reshape(10, 4, 16)).sum(1)
+    assert np.all(np.abs(got - want) <= 2.0 ** -7 * np.abs(want) + 1e-30)
+    h = omoe.bf16_rne(rng.standard_normal((5, 32)).astype(np.float32) * 4)
+    hf = ofp8.bf16_bits_to_f32(h).astype(np.float64)
+    ref = hf[:, :16] / (1 + np.exp(-hf[:, :16])) * hf[:, 16:]
+    np.testing.assert_allclose(omoe.swiglu(h), ref, rtol=1e-6, atol=1e-30)
+    # bf16 RNE ties (engine.py:49 goldens, test_engine.py:49-62)
+    assert list(omoe.bf16_rne(np.array([0x3F808000, 0x3F818000, 0x3F808001], np.uint32).view(np.float32))) == \
+        [0x3F80, 0x3F82, 0x3F81]
