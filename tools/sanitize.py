@@ -36,5 +36,11 @@ tg.quantize_blocks(torch.randn((2, 256, 384), device=dev))
 xc, xs = tg.quantize_col_blocks(torch.randn((m, 256), device=dev), gs)
 dyc, dys = tg.quantize_col_blocks(torch.randn((m, 128), device=dev), gs)
 tg.wgrad_fp8(xc, xs, dyc, dys, gs)
+from paper_2508_16584_b200 import moe  # noqa: E402
+
+h = torch.randn((m + 40, 512), device=dev).to(torch.bfloat16)
+hq, hs = moe.swiglu_quantize(h, gs)
+cc = torch.randn((400, 256), device=dev).to(torch.bfloat16)
+moe.combine(cc, d.dest_rows, torch.rand((100, 4), device=dev))
 torch.cuda.synchronize()
 print("sanitize workload done")
