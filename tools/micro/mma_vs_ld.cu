@@ -282,7 +282,12 @@ int main() {
   cudaMalloc(&g_tr, 6 * 1024 * 8);
   cudaMalloc(&g_sink, (148 * kThreads + 8192) * 4);
   cudaMemset(g_sink, 0, (148 * kThreads + 8192) * 4);
-  run<0, 2, 1, 47>("rot, no drain, 4 stages");
-  run<1, 2, 1, 47>("rot, drain, 4 stages");
+  run<0, 2, 0, 0>("cg2: no drain");
+  run<1, 2, 0, 0>("cg2: 32x32b.x32 drain");
+  run<2, 2, 0, 0>("cg2: 16x256b.x8 drain");
+  run<3, 2, 0, 0>("cg2: 16x128b.x16 drain");
+  run<4, 2, 0, 0>("cg2: 32x32b.x16 drain");
+  run<5, 2, 0, 0>("cg2: 32x32b.x32, half the columns");
+  run<6, 2, 0, 0>("cg2: 32x32b.x32, drain after next MMA");
   return 0;
 }
