@@ -645,6 +645,61 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       const int d = 1 << lg;
       // kBN=256 with epi_passes == 1: one pass, all 8 warps write, chunk 2 half + j / 8
       const int passes = (kBN == 256) ? static_cast<int>(p.epi_passes) : 1;
+      if (kBN == 256 && passes == 1) {
+        // Single pass, the two column halves decoupled: warps of half h write chunks 2h, 2h+1
+        // (their 128 columns), sync only among themselves (named barrier 2 + h, 128 threads),
+        // and their first thread stores them.  A TMA store's smem reads are tracked per
+        // issuing thread, so each half's leader waits for its own earlier stores; the half-tile
+        // path stages in [0, 32 KB) only, i.e. in half 0's chunks, and stores from thread 0.
+        const int hl = 128 * half;  // ptid of this half's leader
+        if (ptid == hl) bulk_wait_read0();
+        named_bar_sync(2 + half, 128);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int chunk = 2 * half + (j >> 3);
+          const int pc = j & 7;
+          const uint32_t w0 = pack_bf16x2(acc[8 * j + 0], acc[8 * j + 1]);
+          const uint32_t w1 = pack_bf16x2(acc[8 * j + 2], acc[8 * j + 3]);
+          const uint32_t w2 = pack_bf16x2(acc[8 * j + 4], acc[8 * j + 5]);
+          const uint32_t w3 = pack_bf16x2(acc[8 * j + 6], acc[8 * j + 7]);
+          const uint32_t c16 = kSwizzleC ? static_cast<uint32_t>(pc ^ (r & 7)) : static_cast<uint32_t>(pc);
+          st_shared_v4(smem_u32(sC + chunk * kChunkBytesC) + static_cast<uint32_t>(r) * 128u + c16 * 16u, w0, w1, w2,
+                       w3);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(2 + half, 128);
+        if (ptid == hl && T.valid > 0 && !prev_grid_done) {
+          griddep_wait();  // WAW on C / tile_map with the previous grid: store only after it completed
+          prev_grid_done = true;
+        }
+        if (ptid == hl && T.valid > 0 && T.n0 + 128 * half < p.N) {
+          for (int ch = 2 * half; ch < 2 * half + 2; ++ch) {
+            const int col = T.n0 + 64 * ch;
+            if (col >= p.N) break;
+            const uint8_t* chunk = sC + ch * kChunkBytesC;
+            tma_store_2d(&p.tmap_c[lg], chunk, col, T.crow0);  // phase a
+            if (T.valid != BM)                                   // phase b (both, even if they coincide)
+              tma_store_2d(&p.tmap_c[lg], chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
+                           T.crow0 + T.valid - d);
+          }
+          bulk_commit();
+          if (p.tile_map) {
+            int32_t* rec = p.tile_map + ((static_cast<int64_t>(t) * kCG + rank) * 2 + half) * TAGG_TILE_MAP_FIELDS;
+            rec[0] = T.g;
+            rec[1] = T.mt;
+            rec[2] = T.n0 + 128 * half;
+            rec[3] = T.row0;
+            rec[4] = T.valid;
+            rec[5] = d;
+            rec[6] = T.crow0;
+            rec[7] = T.valid - d;
+            rec[8] = T.crow0 + T.valid - d;
+          }
+        }
+        if (tr_a) trace_stamp(p.trace, kEvEpiEnd, tiles_done);
+        ++tiles_done;
+        continue;
+      }
       for (int pass = 0; pass < passes; ++pass) {
         if (ptid == 0) bulk_wait_read0();  // earlier stores have finished reading the staging
         named_bar_sync(1, 32 * kNumPromoWarps);
@@ -708,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       if (tr_a) trace_stamp(p.trace, kEvEpiEnd, tiles_done);
       ++tiles_done;
     }
-    if (ptid == 0) bulk_wait0();
+    if (ptid == 0 || ptid == 128) bulk_wait0();  // both column-half leaders store
   }
 
   // ------------------------------------------------------------ teardown
