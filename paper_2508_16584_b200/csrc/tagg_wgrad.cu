@@ -280,11 +280,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
         if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
         if (++acc_i == kNumAcc) { acc_i = 0; accph ^= 1; }
       }
-      // epilogue: one pass, 4 chunks of 64 columns x 128 rows (64 KB); thread -> chunks
-      // 2 half, 2 half + 1 of its row
-      if (ptid == 0) bulk_wait_read0();
-      named_bar_sync(1, 32 * kPromoWarps);
+      // epilogue: one pass, 4 chunks of 64 columns x 128 rows (64 KB).  The two column halves
+      // are independent: warps of half h write chunks 2h, 2h+1 (their 128 columns), sync only
+      // among themselves (named barrier 2 + h) and their first thread stores them (a TMA
+      // store's smem reads are tracked per issuing thread, so each leader waits for its own).
       {
+        const int hl = 128 * half;
+        if (ptid == hl) bulk_wait_read0();
+        named_bar_sync(2 + half, 128);
         const uint32_t base = smem_u32(smem + p.off_c) + static_cast<uint32_t>(r) * 128u;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
@@ -296,16 +299,16 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           st_shared_v4(base + chunk * kChunkC + static_cast<uint32_t>(((jj & 7) ^ (r & 7)) * 16), w0, w1, w2, w3);
         }
         fence_proxy_async_smem();
-      }
-      named_bar_sync(1, 32 * kPromoWarps);
-      if (ptid == 0 && kr < p.K) {
-        const int row = g * p.K + kr;
-        for (int c = 0; c < 4; ++c)
-          if (n0 + 64 * c < p.N) tma_store_2d(&p.map_dw, smem + p.off_c + c * kChunkC, n0 + 64 * c, row);
-        bulk_commit();
+        named_bar_sync(2 + half, 128);
+        if (ptid == hl && kr < p.K) {
+          const int row = g * p.K + kr;
+          for (int c = 2 * half; c < 2 * half + 2; ++c)
+            if (n0 + 64 * c < p.N) tma_store_2d(&p.map_dw, smem + p.off_c + c * kChunkC, n0 + 64 * c, row);
+          bulk_commit();
+        }
       }
     }
-    if (ptid == 0) bulk_wait0();
+    if (ptid == 0 || ptid == 128) bulk_wait0();  // both column-half leaders issue stores
   }
   __syncwarp();
   tc_fence_before();
