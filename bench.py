@@ -552,6 +552,7 @@ def run_extra(torch, tg, dev, rank, fp8_peak, exact):
     out["quantize_dispatch_dsv3"] = run_quantize_dispatch(torch, tg, dev)
     out["wgrad_dsv3_gateup"] = run_wgrad(torch, tg, dev, fp8_peak)
     out["moe_ffn_dsv3_1gpu"] = run_moe_ffn(torch, tg, dev, fp8_peak)
+    out["dense_fp8_reference_8192"] = run_dense_reference(torch, tg, dev, fp8_peak)
     return out
 
 
@@ -607,6 +608,43 @@ def run_quantize_dispatch(torch, tg, dev, tokens=32768, k=7168, topk=8, experts=
     return {"tokens": tokens, "K": k, "topk": topk, "experts": experts, "ms": ms,
             "algorithmic_bytes": nbytes, "gbs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / peak,
             "hbm_peak_gbs": peak, "note": "route plan (3 launches) + quantize/scatter (1 launch), x resident"}
+
+
+def run_dense_reference(torch, tg, dev, fp8_peak, n=8192, iters=10, warmup=3):
+    """dense FP8 on the same box in the same run.  cuBLAS ``torch._scaled_mm``
+    (e4m3, one scale per tensor, no per-block promotion) against this kernel on one 8192-row
+    group with its 1x128 / 128x128 scales."""
+    g = torch.Generator(device=dev).manual_seed(5)
+    a = (torch.randn((n, n), device=dev, generator=g) * 0.5).to(torch.float8_e4m3fn)
+    bt = (torch.randn((n, n), device=dev, generator=g) * 0.5).to(torch.float8_e4m3fn)
+    one = torch.ones((), device=dev)
+    sa = torch.rand((n, n // 128), device=dev, generator=g) * 1e-2 + 1e-3
+    sb = torch.rand((1, n // 128, n // 128), device=dev, generator=g) * 1e-2 + 1e-3
+    gs = torch.tensor([n], dtype=torch.int32, device=dev)
+    b3 = bt.view(torch.uint8).view(1, n, n)
+    out = torch.empty((n, n), dtype=torch.bfloat16, device=dev)
+
+    def cublas():
+        torch._scaled_mm(a, bt.t(), one, one, out_dtype=torch.bfloat16)
+
+    def ours():
+        tg.grouped_gemm_fp8(a, sa, b3, sb, gs, b_layout="nk", out=out)
+
+    res = {}
+    for name, fn in (("cublas_scaled_mm", cublas), ("this_kernel_blockwise", ours)):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        res[name + "_tflops"] = 2.0 * n ** 3 / (s.elapsed_time(e) / iters * 1e-3) / 1e12
+    res["fp8_peak_used"] = fp8_peak
+    res["note"] = "cuBLAS has per-tensor scales (no promotion); this kernel promotes per 128-K block"
+    return res
 
 
 def run_moe_ffn(torch, tg, dev, fp8_peak, tokens=32768, topk=8, experts=256, hidden=7168, inter=2048, iters=5,
