@@ -700,10 +700,35 @@ def run_moe_ffn(torch, tg, dev, fp8_peak, tokens=32768, topk=8, experts=256, hid
     rows = tokens * topk
     flops = 2.0 * rows * hidden * 2 * inter + 2.0 * rows * inter * hidden
     total = sum(ms)
-    return {"tokens": tokens, "topk": topk, "experts": experts, "hidden": hidden, "intermediate": inter,
-            "ms": total, "tflops": flops / (total * 1e-3) / 1e12, "fp8_peak_frac": flops / (total * 1e-3) / 1e12 / fp8_peak,
-            "breakdown_ms": dict(zip(names, ms)),
-            "note": "all intermediates padding-free (no pad rows, no permutation between the GEMMs)"}
+    res = {"tokens": tokens, "topk": topk, "experts": experts, "hidden": hidden, "intermediate": inter,
+           "ms": total, "tflops": flops / (total * 1e-3) / 1e12, "fp8_peak_frac": flops / (total * 1e-3) / 1e12 / fp8_peak,
+           "breakdown_ms": dict(zip(names, ms)),
+           "note": "all intermediates padding-free (no pad rows, no permutation between the GEMMs)"}
+    # backward: dgrad of both GEMMs (K-major weights), SwiGLU backward (K9), wgrad (K6) of both,
+    # dx via the combine, router-weight grads; 2x the forward FLOPs
+    dy = torch.randn((tokens, hidden), device=dev, generator=g).to(torch.bfloat16)
+    _, ctx = moe.moe_ffn(x, eids, wts, w, save=True)
+    for _ in range(1):
+        moe.moe_ffn_backward(dy, ctx, w)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    bw_iters = 2
+    s.record()
+    for _ in range(bw_iters):
+        grads = moe.moe_ffn_backward(dy, ctx, w)
+    e.record()
+    torch.cuda.synchronize()
+    bw_ms = s.elapsed_time(e) / bw_iters
+    marks = []
+    grads = moe.moe_ffn_backward(dy, ctx, w, marks=marks)
+    torch.cuda.synchronize()
+    breakdown = {marks[i][0]: marks[i - 1][1].elapsed_time(marks[i][1]) for i in range(1, len(marks))}
+    del grads, ctx
+    res["backward"] = {"ms": bw_ms, "tflops": 2 * flops / (bw_ms * 1e-3) / 1e12, "breakdown_ms": breakdown,
+                       "dw_bytes": 2 * experts * hidden * 3 * inter,
+                       "note": "dgrad x2 (b_layout nk), K9, wgrad x2 (K6, column-block quantized operands), "
+                               "dx combine (K8), row gathers (K10), router grads (K11)"}
+    return res
 
 
 def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, warmup=2):

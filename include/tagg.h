@@ -232,7 +232,29 @@ int tagg_version(void);
  * ldh*2, I*2, lda and both bases must be multiples of 16 bytes.
  */
 int tagg_swiglu_quantize(const void* h, int64_t ldh, const int32_t* group_sizes, int G, int64_t m_alloc, int I,
-                         void* a, int64_t lda, float* sa, int32_t* err_flag, void* stream);
+                         void* a, int64_t lda, float* sa, int32_t* err_flag, void* v_out, int64_t ldv,
+                         void* stream);
+/* (v_out: nullable bf16 [m_alloc, I] copy of v, pitch ldv, kept by a training forward for wgrad.) */
+
+/* out[r, :] = bf16(row_weights[r] * src[index[r], :]) for r < rows (row_weights nullable = 1):
+   token rows gathered into the grouped layout, e.g. the backward's dL/dc = w[t,k] * dy[t].
+   bf16, H % 8 == 0, 16-byte aligned bases and pitches. */
+int tagg_gather_scale_rows(const void* src, int64_t lds, const int32_t* index, const float* row_weights, int64_t rows,
+                           int H, void* out, int64_t ldo, void* stream);
+/* Router-weight gradient: out[t*topk + k] = <dy[t, :], c[dest_rows[t*topk + k], :]> in fp32. */
+int tagg_router_grad(const void* dy, int64_t lddy, const void* c, int64_t ldc, const int32_t* dest_rows,
+                     int64_t tokens, int topk, int H, float* out, void* stream);
+/*
+ * Backward of tagg_swiglu_quantize: from the saved gate|up rows h = [g | u] (bf16 [m_alloc, 2I])
+ * and dh = dL/dv (bf16 [m_alloc, I], v = silu(g) * u):
+ *   dg = dh * u * sig(g) * (1 + g * (1 - sig(g))),  du = dh * silu(g)
+ * written as bf16 d[g | u] to dgu (nullable, [m_alloc, 2I]) and row-quantized 1x128 FP8 to a / sa
+ * ([m_alloc, 2I] codes, [m_alloc, 2I/128] scales; dg and du tiles separately): the A operand of the
+ * gate|up dgrad GEMM.  Rows [0, sum M_g) only; I % 128 == 0; 16-byte aligned bases and pitches.
+ */
+int tagg_swiglu_backward_quantize(const void* h, int64_t ldh, const void* dh, int64_t lddh,
+                                  const int32_t* group_sizes, int G, int64_t m_alloc, int I, void* dgu,
+                                  int64_t lddgu, void* a, int64_t lda, float* sa, int32_t* err_flag, void* stream);
 /*
  * Top-k combine of the down GEMM output: out[t, :] = bf16( sum_{k < topk} fl(w[t,k] * c[dest[t*topk+k], :]) ),
  * accumulated in fp32 in k order with separate roundings (no FMA).  dest = the dispatch plan's

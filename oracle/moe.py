@@ -39,3 +39,14 @@ def combine(c_bits: np.ndarray, dest: np.ndarray, w: np.ndarray) -> np.ndarray:
         rows = c[dest.reshape(t, topk)[:, k]]
         acc = (acc + (w[:, k:k + 1].astype(np.float32) * rows).astype(np.float32)).astype(np.float32)
     return bf16_rne(acc)
+
+
+def swiglu_backward(h_bits: np.ndarray, dh_bits: np.ndarray) -> np.ndarray:
+    """d[g | u] in float32 from gate|up rows and dL/d(silu(g) * u) (tagg_moe.cu K9)."""
+    h = bf16_bits_to_f32(h_bits).astype(np.float64)
+    dh = bf16_bits_to_f32(dh_bits).astype(np.float64)
+    i = h.shape[1] // 2
+    g, u = h[:, :i], h[:, i:2 * i]
+    with np.errstate(over="ignore"):
+        sig = 1.0 / (1.0 + np.exp(-g))
+    return np.concatenate([dh * u * sig * (1 + g * (1 - sig)), dh * g * sig], axis=1).astype(np.float32)

@@ -36,8 +36,13 @@ SIGNATURES = {
     "tagg_wgrad_fp8": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_int, c_int, c_int, c_vp, c_vp]),
     "tagg_quantize_blocks": (c_int, [c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp,
                                      c_vp]),
-    "tagg_swiglu_quantize": (c_int, [c_vp, c_i64, c_vp, c_int, c_i64, c_int, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "tagg_swiglu_quantize": (c_int, [c_vp, c_i64, c_vp, c_int, c_i64, c_int, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
+                                     c_vp]),
+    "tagg_gather_scale_rows": (c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_int, c_vp, c_i64, c_vp]),
+    "tagg_router_grad": (c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_int, c_int, c_vp, c_vp]),
     "tagg_combine": (c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_i64, c_vp]),
+    "tagg_swiglu_backward_quantize": (c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_i64, c_int, c_vp, c_i64, c_vp,
+                                              c_i64, c_vp, c_vp, c_vp]),
     "tagg_route_plan": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp]),
     "tagg_route_error": (c_int, [c_vp, c_i64, c_int, c_vp]),
     "tagg_quantize_dispatch": (c_int, [c_vp, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_i64, c_vp, c_vp,

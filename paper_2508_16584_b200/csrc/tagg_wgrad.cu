@@ -392,6 +392,106 @@ __global__ void __launch_bounds__(128) quantize_col_blocks_kernel(const void* __
   if (bad) atomicOr(err, 2);
 }
 
+// Vector form: thread = 8 consecutive columns (16-B bf16 / 32-B f32 loads, 8-B code stores),
+// 64 threads = 512 columns per CTA; the (group, token block) lookup is the same table walk.
+template <bool kBf16>
+__global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* __restrict__ x, int64_t ldx, int cols,
+                                                                    const int32_t* __restrict__ group_sizes, int G,
+                                                                    uint8_t* __restrict__ codes, int64_t ldc,
+                                                                    float* __restrict__ scales, int32_t* err) {
+  __shared__ int32_t s_row0, s_rows, s_tb;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int carry_r = 0, carry_b = 0, found = 0;
+    const int want = blockIdx.y;
+    for (int base = 0; base < G && !found; base += 32) {
+      const int g = base + lane;
+      const int m = (g < G) ? max(0, group_sizes[g]) : 0;
+      const int nb = (m + 127) / 128;
+      int im = m, ib = nb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, im, o);
+        const int b = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) { im += a; ib += b; }
+      }
+      const int b0 = carry_b + ib - nb, r0 = carry_r + im - m;
+      const bool mine = g < G && want >= b0 && want < b0 + nb;
+      if (__ballot_sync(0xffffffffu, mine)) {
+        found = 1;
+        if (mine) {
+          const int j = want - b0;
+          s_row0 = r0 + 128 * j;
+          s_rows = min(128, m - 128 * j);
+          s_tb = want;
+        }
+      }
+      carry_r += __shfl_sync(0xffffffffu, im, 31);
+      carry_b += __shfl_sync(0xffffffffu, ib, 31);
+    }
+    if (!found && lane == 0) s_rows = 0;
+  }
+  __syncthreads();
+  const int rows = s_rows;
+  if (rows <= 0) return;
+  const int64_t row0 = s_row0;
+  const int c0 = (blockIdx.x * 64 + threadIdx.x) * 8;
+  if (c0 >= cols) return;  // cols % 8 == 0 on this path
+  auto load8 = [&](int64_t rr, float (&v)[8]) {
+    if constexpr (kBf16) {
+      const uint4 q = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + rr * ldx + c0);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[2 * j] = __uint_as_float(w[j] << 16);
+        v[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+      }
+    } else {
+      const float4* f = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + rr * ldx + c0);
+      const float4 a = f[0], b = f[1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+  };
+  float amax[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) amax[j] = 0.0f;
+  bool bad = false;
+#pragma unroll 4
+  for (int i = 0; i < rows; ++i) {
+    float v[8];
+    load8(row0 + i, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float m = fabsf(v[j]);
+      bad |= !(m <= 3.402823466e38f);
+      amax[j] = fmaxf(amax[j], m);
+    }
+  }
+  float s[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s[j] = amax[j] > 0.0f ? __fdiv_rn(amax[j], 448.0f) : 1.0f;
+  float4* sdst = reinterpret_cast<float4*>(scales + static_cast<int64_t>(s_tb) * cols + c0);
+  sdst[0] = make_float4(s[0], s[1], s[2], s[3]);
+  sdst[1] = make_float4(s[4], s[5], s[6], s[7]);
+#pragma unroll 4
+  for (int i = 0; i < rows; ++i) {
+    float v[8];
+    load8(row0 + i, v);
+    uint32_t w[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint16_t lo, hi;
+      const float a0 = __fdiv_rn(v[4 * h], s[4 * h]), a1 = __fdiv_rn(v[4 * h + 1], s[4 * h + 1]);
+      const float a2 = __fdiv_rn(v[4 * h + 2], s[4 * h + 2]), a3 = __fdiv_rn(v[4 * h + 3], s[4 * h + 3]);
+      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(a1), "f"(a0));
+      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(a3), "f"(a2));
+      w[h] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    }
+    *reinterpret_cast<uint2*>(codes + (row0 + i) * ldc + c0) = make_uint2(w[0], w[1]);
+  }
+  if (bad) atomicOr(err, 2);
+}
+
 }  // namespace wg
 }  // namespace tagg
 
@@ -412,6 +512,19 @@ extern "C" int tagg_quantize_col_blocks(const void* x, int x_dtype, int64_t m_al
   const int64_t tb = tagg_token_blocks_bound(m_alloc, G);
   if (tb > 65535) return TAGG_ERR_UNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int esz = x_dtype == TAGG_DTYPE_BF16 ? 2 : 4;
+  const bool v8 = cols % 8 == 0 && !(reinterpret_cast<uintptr_t>(x) % 16) && !((ldx * esz) % 16) &&
+                  !(reinterpret_cast<uintptr_t>(codes) % 8) && !(ldc % 8) && !(reinterpret_cast<uintptr_t>(scales) % 16);
+  if (v8) {
+    const dim3 g8(static_cast<unsigned>((cols / 8 + 63) / 64), static_cast<unsigned>(tb));
+    if (x_dtype == TAGG_DTYPE_BF16)
+      wg::quantize_col_blocks_v8_kernel<true><<<g8, 64, 0, st>>>(x, ldx, cols, group_sizes, G,
+                                                                 static_cast<uint8_t*>(codes), ldc, scales, err_flag);
+    else
+      wg::quantize_col_blocks_v8_kernel<false><<<g8, 64, 0, st>>>(x, ldx, cols, group_sizes, G,
+                                                                  static_cast<uint8_t*>(codes), ldc, scales, err_flag);
+    return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
+  }
   const dim3 grid(static_cast<unsigned>((cols + 127) / 128), static_cast<unsigned>(tb));
   if (x_dtype == TAGG_DTYPE_BF16)
     wg::quantize_col_blocks_kernel<true><<<grid, 128, 0, st>>>(x, ldx, cols, group_sizes, G,

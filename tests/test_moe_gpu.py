@@ -43,7 +43,7 @@ def test_swiglu_quantize_matches_oracle(i):
     err = torch.zeros(1, dtype=torch.int32, device=DEV)
     gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
     rc = lib().tagg_swiglu_quantize(ht.data_ptr(), 2 * i, gs.data_ptr(), len(sizes), m_alloc, i, a.data_ptr(), lda,
-                                    sa.data_ptr(), err.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                                    sa.data_ptr(), err.data_ptr(), None, 0, torch.cuda.current_stream().cuda_stream)
     assert rc == 0
     torch.cuda.synchronize()
     got_a, got_s = a.cpu().numpy(), sa.cpu().numpy()
@@ -102,3 +102,111 @@ def test_moe_ffn_matches_the_oracle_chain():
     err = np.abs(got - want) / np.maximum(scale, 1e-30)
     assert err.max() <= 2.0 ** -4, err.max()
     assert err.mean() <= 2.0 ** -9, err.mean()
+
+
+def _dequant_blocks(codes, scales):
+    v = ofp8.DECODE_TABLE[codes].astype(np.float64)
+    e, r, c = v.shape
+    s = np.repeat(np.repeat(scales.astype(np.float64), 128, axis=1), 128, axis=2)[:, :r, :c]
+    return v * s
+
+
+def test_moe_ffn_backward_matches_float64():
+    """moe_ffn(save=True) + moe_ffn_backward against float64 math on the same (dequantized) FP8
+    weights.  Activations and gradients pass through 1x128 / column-block FP8 on the GPU, so
+    each gradient is compared by relative Frobenius error."""
+    rng = np.random.default_rng(8)
+    t, topk, e, hid, inter = 200, 2, 4, 256, 128
+    x = rng.standard_normal((t, hid)).astype(np.float32)
+    eids = np.stack([rng.permutation(e)[:topk] for _ in range(t)]).astype(np.int32)
+    wts = rng.random((t, topk)).astype(np.float32)
+    dy = rng.standard_normal((t, hid)).astype(np.float32)
+    w1 = rng.standard_normal((e, hid, 2 * inter)).astype(np.float32) * 0.08
+    w2 = rng.standard_normal((e, inter, hid)).astype(np.float32) * 0.08
+    c1, s1 = tg.quantize_blocks(torch.from_numpy(w1).to(DEV))
+    c2, s2 = tg.quantize_blocks(torch.from_numpy(w2).to(DEV))
+    weights = moe.ExpertWeights(c1, s1, c2, s2)
+    xb = torch.from_numpy(x).to(DEV).to(torch.bfloat16)
+    y, ctx = moe.moe_ffn(xb, torch.from_numpy(eids).to(DEV), torch.from_numpy(wts).to(DEV), weights, save=True)
+    g = moe.moe_ffn_backward(torch.from_numpy(dy).to(DEV).to(torch.bfloat16), ctx, weights)
+    torch.cuda.synchronize()
+    W1 = _dequant_blocks(c1.cpu().numpy(), s1.cpu().numpy())
+    W2 = _dequant_blocks(c2.cpu().numpy(), s2.cpu().numpy())
+    xr = xb.float().cpu().numpy().astype(np.float64)
+    dyr = torch.from_numpy(dy).to(torch.bfloat16).float().numpy().astype(np.float64)
+    yr = np.zeros((t, hid))
+    dx = np.zeros((t, hid))
+    dW1 = np.zeros_like(W1)
+    dW2 = np.zeros_like(W2)
+    dw = np.zeros((t, topk))
+    for ti in range(t):
+        for k in range(topk):
+            ex = eids[ti, k]
+            z = xr[ti] @ W1[ex]
+            gg, uu = z[:inter], z[inter:]
+            sig = 1 / (1 + np.exp(-gg))
+            v = gg * sig * uu
+            o = v @ W2[ex]
+            yr[ti] += wts[ti, k] * o
+            do = wts[ti, k] * dyr[ti]
+            dv = W2[ex] @ do
+            dz = np.concatenate([dv * uu * sig * (1 + gg * (1 - sig)), dv * gg * sig])
+            dx[ti] += W1[ex] @ dz
+            dW2[ex] += np.outer(v, do)
+            dW1[ex] += np.outer(xr[ti], dz)
+            dw[ti, k] = dyr[ti] @ o
+
+    def rel(got, want):
+        return float(np.linalg.norm(got - want) / np.linalg.norm(want))
+
+    assert rel(y.float().cpu().numpy(), yr) < 0.05
+    assert rel(g.dx.float().cpu().numpy(), dx) < 0.08
+    assert rel(g.dw_gate_up.float().cpu().numpy(), dW1) < 0.08
+    assert rel(g.dw_down.float().cpu().numpy(), dW2) < 0.08
+    assert rel(g.dweights.cpu().numpy(), dw) < 0.08
+
+
+@pytest.mark.parametrize("i", [128, 384])
+def test_swiglu_backward_quantize_matches_oracle(i):
+    rng = np.random.default_rng(i + 1)
+    sizes = (150, 0, 77)
+    m, m_alloc = sum(sizes), 300
+    hb = _bf16_bits(rng.standard_normal((m_alloc, 2 * i)).astype(np.float32) * 2)
+    db = _bf16_bits(rng.standard_normal((m_alloc, i)).astype(np.float32))
+    h = torch.from_numpy(hb.view(np.int16)).to(DEV).view(torch.bfloat16)
+    dh = torch.from_numpy(db.view(np.int16)).to(DEV).view(torch.bfloat16)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    dgu, a, sa = moe.swiglu_backward_quantize(h, dh, gs, check=True)
+    torch.cuda.synchronize()
+    want = omoe.swiglu_backward(hb[:m], db[:m])
+    got = dgu[:m].float().cpu().numpy()
+    np.testing.assert_allclose(got, want, rtol=2.0 ** -7, atol=1e-6 * np.abs(want).max())
+    wc, ws = ofp8.quantize_row_tiles(want)
+    np.testing.assert_allclose(sa[:m].cpu().numpy(), ws, rtol=2.0 ** -6)
+    gc = a[:m].cpu().numpy().astype(np.int16)
+    wc = wc.astype(np.int16)
+    step = np.abs((gc & 0x7F) - (wc & 0x7F))
+    assert np.all((((gc >> 7) == (wc >> 7)) & (step <= 1)) | ((gc & 0x7F) + (wc & 0x7F) <= 1))
+
+
+def test_gather_scale_rows_is_bit_exact_and_router_grad():
+    rng = np.random.default_rng(3)
+    t, topk, h = 97, 4, 384
+    xb = _bf16_bits(rng.standard_normal((t, h)).astype(np.float32))
+    idx = rng.integers(0, t, 500).astype(np.int32)
+    w = rng.random(500).astype(np.float32)
+    x = torch.from_numpy(xb.view(np.int16)).to(DEV).view(torch.bfloat16)
+    got = moe.gather_scale_rows(x, torch.from_numpy(idx).to(DEV), torch.from_numpy(w).to(DEV))
+    want = omoe.bf16_rne(w[:, None] * ofp8.bf16_bits_to_f32(xb)[idx])
+    np.testing.assert_array_equal(got.view(torch.int16).cpu().numpy().view(np.uint16), want)
+    plain = moe.gather_scale_rows(x, torch.from_numpy(idx).to(DEV))
+    np.testing.assert_array_equal(plain.view(torch.int16).cpu().numpy().view(np.uint16), xb[idx])
+    # router grad: <dy[t], c[dest[t*topk+k]]>
+    cb = _bf16_bits(rng.standard_normal((t * topk, h)).astype(np.float32))
+    dest = rng.permutation(t * topk).astype(np.int32)
+    c = torch.from_numpy(cb.view(np.int16)).to(DEV).view(torch.bfloat16)
+    g = moe.router_grad(x, c, torch.from_numpy(dest).to(DEV), topk).cpu().numpy()
+    xf = ofp8.bf16_bits_to_f32(xb).astype(np.float64)
+    cf = ofp8.bf16_bits_to_f32(cb).astype(np.float64)
+    want_g = np.einsum("th,tkh->tk", xf, cf[dest].reshape(t, topk, h))
+    np.testing.assert_allclose(g, want_g, rtol=1e-5, atol=1e-4)
