@@ -79,5 +79,10 @@ for name, sizes, n, k, G in cases:
         run(P, flags, G)
         torch.cuda.synchronize()
         L.tagg_debug_trace(None)
-        report(buf.cpu().numpy(), 8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60, "qdown": 600, "ds": 1000, "dsdown": 1000}[name], f"{name} {label}")
+        import os
+        win = os.environ.get("TRACE_WINDOW")
+        lo, hi = (int(v) for v in win.split(",")) if win else (
+            8 if name == "longk" else 64, {"sq8192": 880, "sweep_r64": 270, "longk": 60, "qdown": 600, "ds": 1000,
+                                           "dsdown": 1000}[name])
+        report(buf.cpu().numpy(), lo, hi, f"{name} {label} [{lo},{hi})")
     del P
