@@ -960,6 +960,9 @@ unsigned long long* g_trace = nullptr;
 // Diagnostics: the next launches stamp clock64 per k-block event of CTAs 0 and 1
 // into buf ([2][10][1024] u64, device); NULL turns tracing off.
 extern "C" void tagg_debug_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
+namespace tagg {
+unsigned long long* debug_trace_buffer() { return g_trace; }
+}  // namespace tagg
 
 // Capacity (records) a tile_map buffer needs: an upper bound valid for every
 // tile shape (one record per 128-row x 128-column store tile, incl. empty pair halves).

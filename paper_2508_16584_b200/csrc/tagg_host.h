@@ -11,4 +11,6 @@ bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, uint32_t rank, const voi
                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw);
 // SM count of the current device (cached); -1 on error.
 int sm_count();
+// Diagnostics trace buffer set by tagg_debug_trace (nullptr when off).
+unsigned long long* debug_trace_buffer();
 }  // namespace tagg

@@ -49,9 +49,19 @@ struct Params {
   const float* sx;            // [TB, K]
   const float* sdy;           // [TB, N]
   const int32_t* group_sizes;
+  unsigned long long* trace;  // diagnostics (TAGG_TRACE builds): clock64 stamps of CTAs 0/1
   int G, K, N, KT, NT;        // KT, NT: 256-wide pair tiles (ceil)
   uint32_t off_a, off_b, off_c, off_s, off_tab, off_bar;
 };
+
+// Diagnostics: the same event layout as the forward kernel's trace (tools/trace_wg.py).
+enum WgEv { kWgMmaTempty = 0, kWgMmaFull, kWgMmaIssued, kWgProdEmpty, kWgPromoFull, kWgPromoFreed, kWgPromoDone,
+            kWgPromoSfull, kWgEpiStart, kWgEpiEnd };
+__device__ __forceinline__ void wg_stamp(unsigned long long* tr, int ev, uint32_t i) {
+#ifdef TAGG_TRACE
+  if (tr != nullptr && blockIdx.x < 2 && i < 1024u) tr[(blockIdx.x * 10 + ev) * 1024 + i] = clock64();
+#endif
+}
 
 // CTA pair (cluster of 2, tcgen05 cta_group::2) per 256 (K) x 256 (N) tile of dW_g: CTA
 // `rank` holds K rows [k0 + 128 rank, +128) of X^T and B columns [n0 + 128 rank, +128)
@@ -122,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     setmaxnreg_dec<72>();
     if (warp == 0) {
       // ====================================================== producer (both CTAs)
-      uint32_t stage = 0, phase = 0, sring = 0, sph = 0;
+      uint32_t stage = 0, phase = 0, sring = 0, sph = 0, piter = 0;
       const uint32_t sA0 = smem_u32(smem + p.off_a), sB0 = smem_u32(smem + p.off_b);
       const uint32_t sS0 = smem_u32(smem + p.off_s);
       for (int t = cid; t < tiles; t += nclusters) {
@@ -145,6 +155,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
           // operands
           mbar_wait_addr(smem_u32(&empty[stage]), phase ^ 1);
+          if (lane == 0) wg_stamp(p.trace, kWgProdEmpty, piter);
+          ++piter;
           const int res = min(BT, m - j * BT);
           const int row0 = off + j * BT;
           const uint32_t a_dst = sA0 + stage * kStageA, b_dst = sB0 + stage * kStageB;
@@ -197,12 +209,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
       // groups of 1 KB; K = 32 tokens per MMA = 32 rows = 4 KB
       const uint64_t a0 = umma_desc_sw128(smem_u32(smem + p.off_a), kStageA, 1024);
       const uint64_t b0 = umma_desc_sw128(smem_u32(smem + p.off_b), kStageB, 1024);
-      uint32_t stage = 0, phase = 0, acc = 0, accph = 0;
+      uint32_t stage = 0, phase = 0, acc = 0, accph = 0, miter = 0;
       for (int t = cid; t < tiles; t += nclusters) {
         const int m = tab_m[t / (p.KT * p.NT)];
         for (int j = 0; j * BT < m; ++j) {
           mbar_wait_addr(smem_u32(&tempty[acc]), accph ^ 1);
+          if (lane == 0) wg_stamp(p.trace, kWgMmaTempty, miter);
           mbar_wait_addr(smem_u32(&full[stage]), phase);
+          if (lane == 0) wg_stamp(p.trace, kWgMmaFull, miter);
           tc_fence_after();
           const uint64_t ad = a0 + ((stage * kStageA) >> 4), bd = b0 + ((stage * kStageB) >> 4);
           if (elect_one()) {
@@ -214,6 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
             mma_commit_addr<2>(smem_u32(&tfull[acc]));
           }
           __syncwarp();
+          if (lane == 0) wg_stamp(p.trace, kWgMmaIssued, miter);
+          ++miter;
           if (++stage == kStages) { stage = 0; phase ^= 1; }
           if (++acc == kNumAcc) { acc = 0; accph ^= 1; }
         }
@@ -230,7 +246,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     const uint32_t sS0 = opaque_u32(smem_u32(smem + p.off_s));
     const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
     const uint32_t sfull0 = opaque_u32(smem_u32(&sfull[0])), sempty0 = opaque_u32(smem_u32(&sempty[0]));
-    uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0;
+    uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0, kiter = 0, tiles_done = 0;
+    const bool tr = p.trace != nullptr && pw == 0 && lane == 0;
     for (int t = cid; t < tiles; t += nclusters) {
       const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
       const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
@@ -241,10 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
       for (int i = 0; i < 128; ++i) acc[i] = 0.0f;
       for (int j = 0; j * BT < m; ++j) {
         mbar_wait_addr(sfull0 + 8 * sring, sph);
+        if (tr) wg_stamp(p.trace, kWgPromoSfull, kiter);
         const uint32_t slot = sS0 + sring * kScaleSlot;
         const float sxk = ld_shared_f32(slot + 4u * r);
         const uint32_t sdy = slot + 512u + 4u * (128u * half);
         mbar_wait_addr(tfull0 + 8 * acc_i, accph);
+        if (tr) wg_stamp(p.trace, kWgPromoFull, kiter);
         tc_fence_after();
         const uint32_t taddr = tmem_base + t_lane + acc_i * 256 + 128u * half;
 #pragma unroll
@@ -256,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_leader_addr(tempty0 + 8 * acc_i);
+            if (tr) wg_stamp(p.trace, kWgPromoFreed, kiter);
           }
 #pragma unroll
           for (int c = 0; c < 64; c += 4) {
@@ -277,9 +297,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_addr(sempty0 + 8 * sring);
+        if (tr) wg_stamp(p.trace, kWgPromoDone, kiter);
+        ++kiter;
         if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
         if (++acc_i == kNumAcc) { acc_i = 0; accph ^= 1; }
       }
+      if (tr) wg_stamp(p.trace, kWgEpiStart, tiles_done);
       // epilogue: one pass, 4 chunks of 64 columns x 128 rows (64 KB).  The two column halves
       // are independent: warps of half h write chunks 2h, 2h+1 (their 128 columns), sync only
       // among themselves (named barrier 2 + h) and their first thread stores them (a TMA
@@ -307,6 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           bulk_commit();
         }
       }
+      if (tr) wg_stamp(p.trace, kWgEpiEnd, tiles_done);
+      ++tiles_done;
     }
     if (ptid == 0 || ptid == 128) bulk_wait0();  // both column-half leaders issue stores
   }
@@ -569,6 +594,7 @@ extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, co
   p.sx = sx;
   p.sdy = sdy;
   p.group_sizes = group_sizes;
+  p.trace = debug_trace_buffer();
   p.G = G;
   p.K = K;
   p.N = N;
