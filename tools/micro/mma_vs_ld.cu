@@ -94,8 +94,12 @@ __global__ void __launch_bounds__(kThreads, 1) bench(int nk, unsigned long long*
   if (warp < 4) {
    if (EXTRA & 4) setmaxnreg_dec<72>();
    if (warp == ((EXTRA & 16) ? 1 : 0) && rank == 0) {
-    const uint32_t idesc = idesc_e4m3_f32(128 * CG, 256, BMN != 0);
-    const uint64_t ad = umma_desc_sw128(smem_u32(sA), 16, 1024);
+    // EXTRA & 64: A MN-major too (128 K-rows of 128 B = this CTA's 128 M rows, K step 4 KB),
+    // the wgrad kernel's operand layout
+    constexpr bool AMN = (EXTRA & 64) != 0;
+    const uint32_t idesc = idesc_e4m3_f32_ab(128 * CG, 256, AMN, BMN != 0);
+    const uint64_t ad = umma_desc_sw128(smem_u32(sA), AMN ? 16384 : 16, 1024);
+    const uint32_t astep = AMN ? 256 : 2;
     // B K-major: 256/CG N-rows of 128 B.  MN-major: 128 K-rows of 128 B (this CTA's 128 N columns), K step 4 KB.
     const uint64_t bd = umma_desc_sw128(smem_u32(sB), BMN ? 16384 : 16, 1024);
     const uint32_t bstep = BMN ? 256 : 2;
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) bench(int nk, unsigned long long*
       if (el) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          mma_f8f6f4<CG>(tmem + b * 256, ad + 3072 * (i % ROT) + 2 * k, bd + 3072 * (i % ROT) + bstep * k, idesc, k > 0);
+          mma_f8f6f4<CG>(tmem + b * 256, ad + 3072 * (i % ROT) + astep * k, bd + 3072 * (i % ROT) + bstep * k, idesc, k > 0);
         if (EXTRA & 1) mma_commit<CG>(&empty[i % NS]);
         mma_commit<CG>(&tfull[b]);
       }
@@ -282,12 +286,10 @@ int main() {
   cudaMalloc(&g_tr, 6 * 1024 * 8);
   cudaMalloc(&g_sink, (148 * kThreads + 8192) * 4);
   cudaMemset(g_sink, 0, (148 * kThreads + 8192) * 4);
-  run<0, 2, 0, 0>("cg2: no drain");
-  run<1, 2, 0, 0>("cg2: 32x32b.x32 drain");
-  run<2, 2, 0, 0>("cg2: 16x256b.x8 drain");
-  run<3, 2, 0, 0>("cg2: 16x128b.x16 drain");
-  run<4, 2, 0, 0>("cg2: 32x32b.x16 drain");
-  run<5, 2, 0, 0>("cg2: 32x32b.x32, half the columns");
-  run<6, 2, 0, 0>("cg2: 32x32b.x32, drain after next MMA");
+  run<0, 2, 0, 0>("cg2: no drain, A K-major, B K-major");
+  run<0, 2, 1, 0>("cg2: no drain, A K-major, B MN-major");
+  run<0, 2, 1, 64>("cg2: no drain, A MN-major, B MN-major");
+  run<1, 2, 1, 0>("cg2: 32x32b.x32 drain, A K, B MN");
+  run<1, 2, 1, 64>("cg2: 32x32b.x32 drain, A MN, B MN");
   return 0;
 }
