@@ -414,3 +414,25 @@ def test_back_to_back_launches_into_one_buffer_keep_stream_order(pdl):
     torch.cuda.synchronize()
     assert torch.equal(out[:ms].view(torch.int16), want_small[:ms].view(torch.int16))
     assert torch.equal(out[ms:].view(torch.int16), want_big[ms:].view(torch.int16))
+
+
+@pytest.mark.parametrize("depth", [1, 3])
+def test_host_batches_depths_and_device_group_sizes(depth):
+    """Slot depth 1 (fully serialized reuse) and 3; group sizes given on the device (the C
+    rows copied back are then all m_alloc rows)."""
+    from paper_2508_16584_b200.hostpipe import HostBatch, run_host_batches
+
+    n, k = 128, 256
+    _, _, bc, bsc = _synthetic((1, 1), n, k, 5)
+    b, sb = _dev(bc), _dev(bsc)
+    batches, wants = [], []
+    for i in range(4):
+        sizes = (50 + 30 * i, 7 * i)
+        ac, asc, _, _ = _synthetic(sizes, n, k, 40 + i)
+        gs_dev = _dev(np.array(sizes, np.int32))
+        out = torch.zeros((sum(sizes), n), dtype=torch.int16).pin_memory()
+        batches.append(HostBatch(torch.from_numpy(ac).pin_memory(), torch.from_numpy(asc).pin_memory(), gs_dev, out))
+        wants.append(tg.grouped_gemm_fp8(_dev(ac), _dev(asc), b, sb, gs_dev).view(torch.int16).cpu())
+    run_host_batches(batches, b, sb, depth=depth).synchronize()
+    for bt, want in zip(batches, wants):
+        assert torch.equal(bt.out, want[:bt.out.shape[0]])
