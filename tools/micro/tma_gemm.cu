@@ -270,9 +270,10 @@ int main() {
   float* sink;
   cudaMalloc(&d_out, 148 * 8);
   cudaMalloc(&sink, 148 * kThreads * 4);
-  run<2, 1>("TMA, drain (early)", p, d_out, sink);
-  run<2, 1, 1>("TMA, drain, +scales (conflicted)", p, d_out, sink);
-  run<2, 1, 9>("TMA, drain, +scales (transposed)", p, d_out, sink);
-  run<2, 1, 15>("TMA, drain, +all (transposed)", p, d_out, sink);
+  run<0, 0>("no TMA, no drain", p, d_out, sink);
+  run<0, 1>("TMA, no drain", p, d_out, sink);
+  run<2, 0>("no TMA, drain (early release)", p, d_out, sink);
+  run<2, 1>("TMA, drain (early release)", p, d_out, sink);
+  run<2, 1, 2>("TMA, drain, + epilogue", p, d_out, sink);
   return 0;
 }
