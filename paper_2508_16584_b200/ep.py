@@ -239,10 +239,9 @@ def pipelined_expert_gemm(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_
     be a row-strided view).  Returns [R, n_out]: every row's output back in local row order.
 
     Codes and scales travel packed in one all-to-all per chunk (K + 4*kb bytes a row, padded
-    to 16).  On CUDA
-    the all-to-alls run on ``comm_stream``: chunk c's GEMM overlaps chunk c+1's dispatch and
-    chunk c-1's combine.  Give the GEMM fewer SMs than the device has (grouped_gemm_fp8
-    ``max_sms``) so the NCCL kernels find room beside its persistent grid.
+    to 16).  On CUDA the all-to-alls run on ``comm_stream``: chunk c's GEMM overlaps chunk
+    c+1's dispatch and chunk c-1's combine.  Give the GEMM fewer SMs than the device has
+    (grouped_gemm_fp8 ``max_sms``) so the NCCL kernels find room beside its persistent grid.
     """
     if a_codes.dtype == torch.float8_e4m3fn:
         a_codes = a_codes.view(torch.uint8)
