@@ -314,6 +314,36 @@ def run_problem_set(torch, tg, prob, iters, warmup, flush=None, exact=False):
     return {k: flops / (v * 1e-3) / 1e12 for k, v in res.items()}, res, ws.nbytes()
 
 
+def per_residue_speedups(torch, tg, prob, iters=3):
+    """Speedup over pad + padded for EVERY residue r of the sweep (the north star's "beats
+    pad+padded across the residual sweep"): each size vector timed alone, both paths, with and
+    without the unpad copy.  Back-to-back launches of one size vector (events around them)."""
+    ws = tg.PaddedWorkspace(prob.m_alloc, prob.G, prob.k, prob.n, prob.a.device)
+
+    def timed(fn):
+        fn()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / iters
+
+    sp, sp_nu = [], []
+    for gs in prob.gs:
+        t_a = timed(lambda: tg.grouped_gemm_fp8(prob.a, prob.sa, prob.b, prob.sb, gs, out=prob.out))
+        t_p = timed(lambda: tg.padded_grouped_gemm_fp8(prob.a, prob.sa, prob.b, prob.sb, gs, ws, out=prob.out))
+        t_n = timed(lambda: tg.padded_grouped_gemm_fp8(prob.a, prob.sa, prob.b, prob.sb, gs, ws, out=prob.out,
+                                                       unpad=False))
+        sp.append(t_p / t_a)
+        sp_nu.append(t_n / t_a)
+    worst = min(range(len(sp)), key=lambda i: sp_nu[i])
+    return {"min": min(sp), "max": max(sp), "min_no_unpad": min(sp_nu), "max_no_unpad": max(sp_nu),
+            "r_of_min_no_unpad": worst + 1, "all_above_1": bool(min(sp_nu) > 1.0),
+            "per_r_no_unpad": [round(x, 3) for x in sp_nu]}
+
+
 def measured_peak_deltas(torch, tg, prob, sizes):
     """the allocator's peak-memory delta of one call of each path (outputs,
     workspace and all), on the largest size vector of the sweep."""
@@ -420,6 +450,7 @@ def main():
     base_tf, base_ms, ws_bytes = run_problem_set(torch, tg, P, iters=max(2, args.steps // 2), warmup=1,
                                                  exact=args.exact)
     mem_measured = measured_peak_deltas(torch, tg, P, P.sizes_list[0])
+    per_r = per_residue_speedups(torch, tg, P)
     acc = [tg.account(s, 4096, 7168) for s in P.sizes_list]
     saved_pct = 100.0 * (1 - sum(a.bytes_actual for a in acc) / sum(a.bytes_padded for a in acc))
 
@@ -502,6 +533,7 @@ def main():
         "speedup_vs_padded_no_unpad": base_ms["padded_no_unpad"] / base_ms["adaptive"],
         "padded_baseline": {"value": base_tf["padded"], "value_no_unpad": base_tf["padded_no_unpad"], "unit": UNIT,
                             "workspace_bytes": ws_bytes},
+        "speedup_vs_padded_per_r": per_r,
         "memory_saved_pct": saved_pct,
         "memory_measured": mem_measured,
         "fp8_peak_frac": {"of_2x_measured_bf16": value / world / fp8_peak, "of_spec_4500": value / world / FP8_SPEC_TFLOPS},
