@@ -585,6 +585,7 @@ def run_extra(torch, tg, dev, rank, fp8_peak, exact):
     out["wgrad_dsv3_gateup"] = run_wgrad(torch, tg, dev, fp8_peak)
     out["moe_ffn_dsv3_1gpu"] = run_moe_ffn(torch, tg, dev, fp8_peak)
     out["dense_fp8_reference_8192"] = run_dense_reference(torch, tg, dev, fp8_peak)
+    out["skinny_sweep"] = run_skinny(torch, tg, dev)
     return out
 
 
@@ -640,6 +641,37 @@ def run_quantize_dispatch(torch, tg, dev, tokens=32768, k=7168, topk=8, experts=
     return {"tokens": tokens, "K": k, "topk": topk, "experts": experts, "ms": ms,
             "algorithmic_bytes": nbytes, "gbs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / peak,
             "hbm_peak_gbs": peak, "note": "route plan (3 launches) + quantize/scatter (1 launch), x resident"}
+
+
+def run_skinny(torch, tg, dev, iters=10):
+    """SURVEY.md §8d, configs[1] variant "skinny": 8 groups of M_g = r rows (N=4096, K=7168,
+    per-expert B [8, 7168, 4096]).  HBM-bound: every launch streams all of B (235 MB) for
+    8r rows, so the roofline is achieved GB/s of the algorithmic bytes."""
+    hbm = _peaks()[0]["hbm_gbs"]
+    res = []
+    for r in (1, 8, 32, 64, 127):
+        P = Problem(torch, f"skinny_r{r}", [tuple([r] * 8)], 4096, 7168, 8, dev, seed=r)
+        gs = P.gs[0]
+        ws = tg.PaddedWorkspace(P.m_alloc, P.G, P.k, P.n, dev)
+
+        def timed(fn):
+            for _ in range(3):
+                fn()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(iters):
+                fn()
+            e.record()
+            torch.cuda.synchronize()
+            return s.elapsed_time(e) / iters
+
+        t = timed(lambda: tg.grouped_gemm_fp8(P.a, P.sa, P.b, P.sb, gs, out=P.out))
+        tp = timed(lambda: tg.padded_grouped_gemm_fp8(P.a, P.sa, P.b, P.sb, gs, ws, out=P.out))
+        nbytes = P.algorithmic_bytes(P.sizes_list[0])
+        res.append({"r": r, "us": t * 1e3, "gbs": nbytes / t / 1e6, "hbm_frac": nbytes / t / 1e6 / hbm,
+                    "tflops": P.flops[0] / (t * 1e-3) / 1e12, "speedup_vs_padded": tp / t})
+        del P, ws
+    return {"groups": 8, "N": 4096, "K": 7168, "hbm_peak_gbs": hbm, "per_r": res}
 
 
 def run_dense_reference(torch, tg, dev, fp8_peak, n=8192, iters=10, warmup=3):

@@ -57,7 +57,10 @@ extern "C" {
                                         default CTA-pair tile (cta_group::2) */
 #define TAGG_FLAG_TILE_N128 8u       /* CTA-pair tile 256x128 (more, smaller tiles: fewer idle SMs
                                         in the last wave of small problems) */
-#define TAGG_FLAG_TILE_N256 16u      /* CTA-pair tile 256x256 (the default) */
+#define TAGG_FLAG_TILE_N256 16u      /* CTA-pair tile 256x256.  With none of SINGLE_CTA / TILE_N128 /
+                                        TILE_N256 set, the launch picks 256x256 pair tiles, or 1-CTA
+                                        128x128 tiles when 3 G <= m_alloc <= 128 G (HBM-bound skinny
+                                        groups) */
 #define TAGG_FLAG_SERIAL 32u         /* no programmatic dependent launch.  By default a grouped GEMM
                                         is launched with PDL: when the previous kernel in the stream
                                         is a grouped GEMM, this one's CTAs start on the SMs that grid

@@ -986,9 +986,21 @@ static int launch_sms(uint32_t flags, int cg) {
   return cap < cg ? 0 : std::min(sms, cap);
 }
 
+// Tile shape without an explicit TAGG_FLAG_SINGLE_CTA / _TILE_N128 / _TILE_N256: the CTA-pair
+// 256x256 tile, unless the groups average 3..128 rows (3 G <= m_alloc <= 128 G).  Such
+// launches are HBM-bound (every group streams its whole B for a few rows), and 1-CTA 128x128
+// tiles spread the B stream over twice the tiles: 77-82% of HBM bandwidth instead of 68-70%
+// on the skinny sweep (bench.py extra skinny_sweep, tools/skinny_tiles.py).  Below 3 rows per
+// group the pair tile measured faster (54 vs 62 us at 1-2 rows).
+static bool auto_single_cta(int64_t m_alloc, int G, uint32_t flags) {
+  if (flags & (TAGG_FLAG_SINGLE_CTA | TAGG_FLAG_TILE_N128 | TAGG_FLAG_TILE_N256))
+    return (flags & TAGG_FLAG_SINGLE_CTA) != 0;
+  return m_alloc >= 3ll * G && m_alloc <= static_cast<int64_t>(BM) * G;
+}
+
 extern "C" int tagg_launch_clusters(int64_t m_alloc, int G, int N, uint32_t flags) {
   if (m_alloc < 0 || G < 1 || N < 64) return TAGG_ERR_CONFIG;
-  const int cg = (flags & TAGG_FLAG_SINGLE_CTA) ? 1 : 2;
+  const int cg = auto_single_cta(m_alloc, G, flags) ? 1 : 2;
   const int sms = launch_sms(flags, cg);
   if (sms < 0) return TAGG_ERR_CUDA;
   if (sms == 0) return TAGG_ERR_CONFIG;
@@ -1028,7 +1040,7 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   // whose 320 pair tiles leave the last of 5 waves 32% full), or an explicit
   // 256x128 pair tile / 1-CTA 128x128 tile.
   int cg = 2, bn = 256;
-  if (flags & TAGG_FLAG_SINGLE_CTA) {
+  if (auto_single_cta(m_alloc, G, flags)) {
     cg = 1;
     bn = 128;
   } else if (flags & TAGG_FLAG_TILE_N128) {

@@ -185,7 +185,8 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
     Returns ``out`` (bf16 [c_rows, N]).  Only rows of valid group rows are
     written; with ``c_row_offsets`` (int64 CUDA [G]) group g's rows start at
     c_row_offsets[g].  ``tile`` picks the tile shape: "pair_n256" (CTA pair,
-    256x256), "pair_n128" (CTA pair, 256x128), "1cta" (128x128) or None/"auto".
+    256x256), "pair_n128" (CTA pair, 256x128), "1cta" (128x128) or None/"auto" (pair 256x256,
+    or 1-CTA tiles when 3 G <= m_alloc <= 128 G: skinny, HBM-bound groups).
     """
     if not (isinstance(a, torch.Tensor) and a.is_cuda):
         raise ValueError("grouped_gemm_fp8 expects CUDA tensors (no CPU fallback)")

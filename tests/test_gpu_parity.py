@@ -45,9 +45,9 @@ def test_golden_fixtures(name, mode):
 
 
 def _pairs(sizes, n):
-    """CTA pairs of a default-tile launch over these groups (tagg_launch_clusters)."""
+    """CTA pairs of a 256x256 pair-tile launch over these groups (tagg_launch_clusters)."""
     from paper_2508_16584_b200._lib import lib
-    return lib().tagg_launch_clusters(int(sum(sizes)), len(sizes), n, 0)
+    return lib().tagg_launch_clusters(int(sum(sizes)), len(sizes), n, 16)
 
 
 
@@ -324,7 +324,7 @@ def test_thousands_of_groups_mostly_empty():
     m = sum(sizes)
     tmap = torch.full((tg.max_tiles(m, len(sizes), n), 9), -1, dtype=torch.int32, device=DEV)
     out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
-                              tile_map=tmap)
+                              tile_map=tmap, tile="pair_n256")
     got = out.view(torch.int16).cpu().numpy().view(np.uint16)
     assert_parity(got, oracle_c(ac, asc, bc, bsc, sizes), label="G=4096")
     tm = tmap.cpu().numpy()
@@ -436,3 +436,24 @@ def test_host_batches_depths_and_device_group_sizes(depth):
     run_host_batches(batches, b, sb, depth=depth).synchronize()
     for bt, want in zip(batches, wants):
         assert torch.equal(bt.out, want[:bt.out.shape[0]])
+
+
+def test_auto_tile_picks_1cta_for_skinny_groups():
+    """tile=None: 1-CTA 128x128 tiles when 3 G <= m_alloc <= 128 G (the tile map shows the
+    128x128 schedule), the CTA pair otherwise; values match the oracle either way."""
+    from paper_2508_16584_b200._lib import lib
+
+    n, k = 256, 384
+    for sizes in ((5, 100, 0, 120), (300, 129, 2), (1, 2, 0, 1)):
+        ac, asc, bc, bsc = _synthetic(sizes, n, k, sum(sizes))
+        m = sum(sizes)
+        tmap = torch.full((tg.max_tiles(m, len(sizes), n), 9), -1, dtype=torch.int32, device=DEV)
+        out = tg.grouped_gemm_fp8(_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)),
+                                  tile_map=tmap)
+        assert_parity(out.view(torch.int16).cpu().numpy().view(np.uint16), oracle_c(ac, asc, bc, bsc, sizes))
+        tm = tmap.cpu().numpy()
+        tm = sorted(tuple(int(x) for x in r) for r in tm[tm[:, 0] >= 0])
+        skinny = 3 * len(sizes) <= m <= 128 * len(sizes)
+        clusters = lib().tagg_launch_clusters(m, len(sizes), n, 0)
+        tile = "1cta" if skinny else "pair_n256"
+        assert tm == sorted(oplan.kernel_tile_map(sizes, n, tile, num_pairs=clusters))
