@@ -66,3 +66,31 @@ def test_op_matches_the_wrapper():
     c1, s1 = torch.ops.tagg.quantize_row_tiles(x)
     c2, s2 = tg.quantize_row_tiles(x)
     assert torch.equal(c1, c2) and torch.equal(s1, s2)
+
+
+def test_product_paths_refuse_cpu_tensors():
+    """No CPU fallback anywhere on the product path: CPU tensors raise before any work."""
+    from paper_2508_16584_b200 import InvalidInput, ShapeMismatch, moe, quant
+    from paper_2508_16584_b200.hostpipe import HostBatch, run_host_batches
+
+    x = torch.zeros((4, 256), dtype=torch.bfloat16)
+    gs = torch.tensor([4], dtype=torch.int32)
+    with pytest.raises(InvalidInput):
+        moe.swiglu_quantize(x, gs)
+    with pytest.raises(InvalidInput):
+        moe.swiglu_backward_quantize(torch.zeros((4, 256), dtype=torch.bfloat16), torch.zeros((4, 128),
+                                                                                            dtype=torch.bfloat16), gs)
+    with pytest.raises(InvalidInput):
+        moe.combine(x, torch.zeros(4, dtype=torch.int32), torch.ones((4, 1)))
+    with pytest.raises(ShapeMismatch):
+        moe.gather_scale_rows(x, torch.zeros(2, dtype=torch.int32))
+    with pytest.raises(InvalidInput):
+        quant.quantize_row_tiles(x)
+    with pytest.raises(InvalidInput):
+        quant.route_plan(torch.zeros(4, dtype=torch.int32), 2)
+    with pytest.raises(ValueError):
+        tg.grouped_gemm_fp8(torch.zeros((4, 128), dtype=torch.uint8), torch.ones((4, 1)),
+                            torch.zeros((1, 128, 64), dtype=torch.uint8), torch.ones((1, 1, 1)), gs)
+    with pytest.raises((ValueError, RuntimeError, AssertionError, AttributeError, ShapeMismatch)):
+        run_host_batches([HostBatch(x, x, gs, x)], torch.zeros((1, 128, 64), dtype=torch.uint8),
+                         torch.ones((1, 1, 1)), depth=0)
