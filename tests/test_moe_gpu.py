@@ -210,3 +210,42 @@ def test_gather_scale_rows_is_bit_exact_and_router_grad():
     cf = ofp8.bf16_bits_to_f32(cb).astype(np.float64)
     want_g = np.einsum("th,tkh->tk", xf, cf[dest].reshape(t, topk, h))
     np.testing.assert_allclose(g, want_g, rtol=1e-5, atol=1e-4)
+
+
+def test_moe_ffn_forward_is_graph_capturable():
+    """The whole padding-free MoE FFN forward has no host sync: it captures into one CUDA graph,
+    and replays with new activations and new routing match eager calls bit for bit."""
+    rng = np.random.default_rng(12)
+    t, topk, e, hid, inter = 256, 4, 8, 256, 128
+    w1 = torch.from_numpy(rng.standard_normal((e, hid, 2 * inter)).astype(np.float32) * 0.1).to(DEV)
+    w2 = torch.from_numpy(rng.standard_normal((e, inter, hid)).astype(np.float32) * 0.1).to(DEV)
+    c1, s1 = tg.quantize_blocks(w1)
+    c2, s2 = tg.quantize_blocks(w2)
+    weights = moe.ExpertWeights(c1, s1, c2, s2)
+
+    def inputs(seed):
+        r = np.random.default_rng(seed)
+        x = torch.from_numpy(r.standard_normal((t, hid)).astype(np.float32)).to(DEV).to(torch.bfloat16)
+        ids = torch.from_numpy(np.stack([r.permutation(e)[:topk] for _ in range(t)]).astype(np.int32)).to(DEV)
+        wt = torch.from_numpy(r.random((t, topk)).astype(np.float32)).to(DEV)
+        return x, ids, wt
+
+    x, ids, wt = inputs(0)
+    moe.moe_ffn(x, ids, wt, weights)  # warm-up outside capture (allocator, tensor maps)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            y = moe.moe_ffn(x, ids, wt, weights)
+    torch.cuda.current_stream().wait_stream(side)
+    for seed in (1, 2):
+        nx, nids, nwt = inputs(seed)
+        x.copy_(nx)
+        ids.copy_(nids)
+        wt.copy_(nwt)
+        graph.replay()
+        want = moe.moe_ffn(nx, nids, nwt, weights)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int16), want.view(torch.int16)), seed
