@@ -190,6 +190,12 @@ int64_t tagg_token_blocks_bound(int64_t m_alloc, int G);
 int tagg_quantize_col_blocks(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
                              const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
                              int32_t* err_flag, void* stream);
+/* The same with a row gather: grouped row r is row_weights[r] * x[index[r], :] (row_weights
+   nullable = 1), for rows grouped rows; x is token-ordered (e.g. activations or dL/dy), so no
+   grouped copy is materialized.  Needs cols % 8 == 0 and 16-byte aligned x rows. */
+int tagg_quantize_col_blocks_gather(const void* x, int x_dtype, int64_t ldx, const int32_t* index,
+                                    const float* row_weights, int64_t rows, int cols, const int32_t* group_sizes,
+                                    int G, void* codes, int64_t ldc, float* scales, int32_t* err_flag, void* stream);
 /*
  * dW_g = X_g^T dY_g for every group (K % 128 == 0, N % 128 == 0): x [m_alloc, K] and
  * dy [m_alloc, N] e4m3 codes in the padding-free grouped layout (dense rows), sx [TB, K]

@@ -33,6 +33,8 @@ SIGNATURES = {
     "tagg_token_blocks_bound": (c_i64, [c_i64, c_int]),
     "tagg_quantize_col_blocks": (c_int, [c_vp, c_int, c_i64, c_int, c_i64, c_vp, c_int, c_vp, c_i64, c_vp, c_vp,
                                          c_vp]),
+    "tagg_quantize_col_blocks_gather": (c_int, [c_vp, c_int, c_i64, c_vp, c_vp, c_i64, c_int, c_vp, c_int, c_vp,
+                                                c_i64, c_vp, c_vp, c_vp]),
     "tagg_wgrad_fp8": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_int, c_int, c_int, c_vp, c_vp]),
     "tagg_quantize_blocks": (c_int, [c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp,
                                      c_vp]),

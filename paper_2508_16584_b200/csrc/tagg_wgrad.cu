@@ -420,10 +420,14 @@ __global__ void __launch_bounds__(128) quantize_col_blocks_kernel(const void* __
 // Vector form: thread = 8 consecutive columns (16-B bf16 / 32-B f32 loads, 8-B code stores),
 // 64 threads = 512 columns per CTA; the (group, token block) lookup is the same table walk.
 template <bool kBf16>
+// Optional gather: grouped row r reads row_weights[r] * x[index[r]] (index / row_weights
+// nullable), so token-ordered activations are quantized into the grouped layout without a copy.
 __global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* __restrict__ x, int64_t ldx, int cols,
                                                                     const int32_t* __restrict__ group_sizes, int G,
                                                                     uint8_t* __restrict__ codes, int64_t ldc,
-                                                                    float* __restrict__ scales, int32_t* err) {
+                                                                    float* __restrict__ scales, int32_t* err,
+                                                                    const int32_t* __restrict__ index,
+                                                                    const float* __restrict__ row_weights) {
   __shared__ int32_t s_row0, s_rows, s_tb;
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -462,7 +466,9 @@ __global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* 
   const int64_t row0 = s_row0;
   const int c0 = (blockIdx.x * 64 + threadIdx.x) * 8;
   if (c0 >= cols) return;  // cols % 8 == 0 on this path
-  auto load8 = [&](int64_t rr, float (&v)[8]) {
+  auto load8 = [&](int64_t r_grouped, float (&v)[8]) {
+    const int64_t rr = index ? static_cast<int64_t>(index[r_grouped]) : r_grouped;
+    const float wr = row_weights ? row_weights[r_grouped] : 1.0f;
     if constexpr (kBf16) {
       const uint4 q = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + rr * ldx + c0);
       const uint32_t w[4] = {q.x, q.y, q.z, q.w};
@@ -475,6 +481,10 @@ __global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* 
       const float4* f = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + rr * ldx + c0);
       const float4 a = f[0], b = f[1];
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+    if (row_weights) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __fmul_rn(wr, v[j]);
     }
   };
   float amax[8];
@@ -527,9 +537,32 @@ extern "C" int64_t tagg_token_blocks_bound(int64_t m_alloc, int G) {
   return (m_alloc + 127) / 128 + G;
 }
 
+static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
+                                    const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
+                                    int32_t* err_flag, const int32_t* index, const float* row_weights, void* stream);
+
 extern "C" int tagg_quantize_col_blocks(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
                                         const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
                                         int32_t* err_flag, void* stream) {
+  return quantize_col_blocks_impl(x, x_dtype, m_alloc, cols, ldx, group_sizes, G, codes, ldc, scales, err_flag,
+                                  nullptr, nullptr, stream);
+}
+
+extern "C" int tagg_quantize_col_blocks_gather(const void* x, int x_dtype, int64_t ldx, const int32_t* index,
+                                               const float* row_weights, int64_t rows, int cols,
+                                               const int32_t* group_sizes, int G, void* codes, int64_t ldc,
+                                               float* scales, int32_t* err_flag, void* stream) {
+  if (rows > 0 && !index) return TAGG_ERR_SHAPE;
+  if (cols % 8 || (reinterpret_cast<uintptr_t>(x) % 16) || ((ldx * (x_dtype == TAGG_DTYPE_BF16 ? 2 : 4)) % 16) ||
+      (reinterpret_cast<uintptr_t>(codes) % 8) || (ldc % 8) || (reinterpret_cast<uintptr_t>(scales) % 16))
+    return TAGG_ERR_ALIGNMENT;  // the gather form is the vector kernel only
+  return quantize_col_blocks_impl(x, x_dtype, rows, cols, ldx, group_sizes, G, codes, ldc, scales, err_flag, index,
+                                  row_weights, stream);
+}
+
+static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
+                                    const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
+                                    int32_t* err_flag, const int32_t* index, const float* row_weights, void* stream) {
   if (x_dtype != TAGG_DTYPE_BF16 && x_dtype != TAGG_DTYPE_F32) return TAGG_ERR_CONFIG;
   if (G < 1 || cols < 1 || m_alloc < 0 || ldx < cols || ldc < cols) return TAGG_ERR_SHAPE;
   if (m_alloc == 0) return TAGG_OK;
@@ -544,10 +577,12 @@ extern "C" int tagg_quantize_col_blocks(const void* x, int x_dtype, int64_t m_al
     const dim3 g8(static_cast<unsigned>((cols / 8 + 63) / 64), static_cast<unsigned>(tb));
     if (x_dtype == TAGG_DTYPE_BF16)
       wg::quantize_col_blocks_v8_kernel<true><<<g8, 64, 0, st>>>(x, ldx, cols, group_sizes, G,
-                                                                 static_cast<uint8_t*>(codes), ldc, scales, err_flag);
+                                                                 static_cast<uint8_t*>(codes), ldc, scales, err_flag,
+                                                                 index, row_weights);
     else
       wg::quantize_col_blocks_v8_kernel<false><<<g8, 64, 0, st>>>(x, ldx, cols, group_sizes, G,
-                                                                  static_cast<uint8_t*>(codes), ldc, scales, err_flag);
+                                                                  static_cast<uint8_t*>(codes), ldc, scales, err_flag,
+                                                                  index, row_weights);
     return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
   }
   const dim3 grid(static_cast<unsigned>((cols + 127) / 128), static_cast<unsigned>(tb));

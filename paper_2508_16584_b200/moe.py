@@ -218,13 +218,12 @@ def moe_ffn_backward(dy: torch.Tensor, ctx: MoeContext, w: ExpertWeights, *, mar
     dx = combine(dxd, d.dest_rows, torch.ones((t, topk), dtype=torch.float32, device=dy.device))
     _mark(marks, "dx_combine")
     # wgrad: dW_down = H2^T dC, dW_gu = X^T dGU, per group
-    xs = gather_scale_rows(ctx.x, src)
     hq, hs = quantize_col_blocks(ctx.v, gs)
-    cq, cs = quantize_col_blocks(dc, gs)
+    cq, cs = quantize_col_blocks(dy, gs, index=src, row_weights=w_rows)  # w[t,k] dy[t], gathered in place
     _mark(marks, "wgrad_down_quantize")
     dw_down = wgrad_fp8(hq, hs, cq, cs, gs)
     _mark(marks, "wgrad_down")
-    xq, xsc = quantize_col_blocks(xs, gs)
+    xq, xsc = quantize_col_blocks(ctx.x, gs, index=src)                # x[t], gathered in place
     gq, gsc = quantize_col_blocks(dgu, gs)
     _mark(marks, "wgrad_gate_up_quantize")
     dw_gate_up = wgrad_fp8(xq, xsc, gq, gsc, gs)

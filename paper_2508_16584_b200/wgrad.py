@@ -16,12 +16,17 @@ from .errors import InvalidInput, ShapeMismatch, raise_for_status
 from .quant import _DTYPES, _check_cuda, _stream
 
 
-def quantize_col_blocks(x: torch.Tensor, group_sizes: torch.Tensor, *, check: bool = False):
+def quantize_col_blocks(x: torch.Tensor, group_sizes: torch.Tensor, *, check: bool = False,
+                        index: torch.Tensor | None = None, row_weights: torch.Tensor | None = None):
     """(codes uint8 [M, C], scales f32 [TB_bound, C]) for x [M, C] in the grouped layout.
 
     Scale row tb holds the tb-th (group, 128-token block) in group order; only the first
     sum(ceil(M_g/128)) rows are defined (group sizes stay on the device: no host sync).
+    With ``index`` (int [M]), grouped row r is ``row_weights[r] * x[index[r]]`` (weights
+    optional): token-ordered rows are quantized into the grouped layout without a copy.
     """
+    if index is not None:
+        return _quantize_col_blocks_gather(x, group_sizes, index, row_weights, check)
     _check_cuda(x, "x")
     if x.dim() != 2:
         raise InvalidInput("expected a 2-D matrix")
@@ -40,6 +45,29 @@ def quantize_col_blocks(x: torch.Tensor, group_sizes: torch.Tensor, *, check: bo
     rc = lib().tagg_quantize_col_blocks(x.data_ptr(), _DTYPES[x.dtype], m, c, x.stride(0), group_sizes.data_ptr(),
                                         g, codes.data_ptr(), c, scales.data_ptr(), err.data_ptr(), _stream())
     raise_for_status(rc, "tagg_quantize_col_blocks")
+    if check and int(err.item()):
+        raise InvalidInput("matrix entries must be finite")
+    return codes, scales
+
+
+def _quantize_col_blocks_gather(x, group_sizes, index, row_weights, check):
+    _check_cuda(x, "x")
+    if x.dim() != 2 or x.dtype not in _DTYPES or x.stride(1) != 1:
+        raise ShapeMismatch("x must be a row-major bf16 / f32 matrix")
+    if group_sizes.dtype != torch.int32 or not group_sizes.is_cuda:
+        raise ShapeMismatch("group_sizes must be an int32 CUDA tensor")
+    idx = index.to(torch.int32).contiguous()
+    w = None if row_weights is None else row_weights.to(torch.float32).contiguous()
+    m, c = idx.numel(), x.shape[1]
+    g = group_sizes.numel()
+    tb = lib().tagg_token_blocks_bound(m, g)
+    codes = torch.empty((m, c), dtype=torch.uint8, device=x.device)
+    scales = torch.empty((max(tb, 1), c), dtype=torch.float32, device=x.device)
+    err = torch.zeros(1, dtype=torch.int32, device=x.device)
+    rc = lib().tagg_quantize_col_blocks_gather(x.data_ptr(), _DTYPES[x.dtype], x.stride(0), idx.data_ptr(),
+                                               None if w is None else w.data_ptr(), m, c, group_sizes.data_ptr(), g,
+                                               codes.data_ptr(), c, scales.data_ptr(), err.data_ptr(), _stream())
+    raise_for_status(rc, "tagg_quantize_col_blocks_gather")
     if check and int(err.item()):
         raise InvalidInput("matrix entries must be finite")
     return codes, scales

@@ -81,3 +81,25 @@ def test_wgrad_never_reads_the_next_group():
     again = tg.wgrad_fp8(xc2, xs, dc2, ds, gs)[0]
     torch.cuda.synchronize()
     assert torch.equal(base.view(torch.int16), again.view(torch.int16))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_col_block_gather_equals_quantizing_the_gathered_copy(dtype):
+    """quantize_col_blocks(x, index=, row_weights=) is bit-identical to quantizing the gathered,
+    scaled copy fl(w[r] * x[index[r]])."""
+    torch.manual_seed(4)
+    t, c = 150, 256
+    sizes = (130, 0, 77, 1)
+    x = (torch.randn((t, c), device=DEV) * 3).to(dtype)
+    idx = torch.randint(0, t, (sum(sizes),), device=DEV, dtype=torch.int32)
+    w = torch.rand(sum(sizes), device=DEV)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    got_c, got_s = tg.quantize_col_blocks(x, gs, index=idx, row_weights=w)
+    copy = (x.float().index_select(0, idx.long()) * w[:, None])
+    want_c, want_s = tg.quantize_col_blocks(copy, gs)
+    tb = sum(-(-s // 128) for s in sizes)
+    assert torch.equal(got_c, want_c)
+    assert torch.equal(got_s[:tb], want_s[:tb])
+    plain_c, plain_s = tg.quantize_col_blocks(x, gs, index=idx)
+    want_pc, want_ps = tg.quantize_col_blocks(x.index_select(0, idx.long()).contiguous(), gs)
+    assert torch.equal(plain_c, want_pc) and torch.equal(plain_s[:tb], want_ps[:tb])
