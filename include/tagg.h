@@ -64,11 +64,16 @@ extern "C" {
 #define TAGG_FLAG_SERIAL 32u         /* no programmatic dependent launch.  By default a grouped GEMM
                                         is launched with PDL: when the previous kernel in the stream
                                         is a grouped GEMM, this one's CTAs start on the SMs that grid
-                                        releases and run their main loop; they wait for its completion
-                                        (griddepcontrol.wait) only before their first global store.
-                                        So its inputs must not be written by the grouped GEMM launched
-                                        right before it (any other kernel in between restores full
-                                        ordering: it triggers only at completion). */
+                                        releases, initialise their barriers and TMEM, and then wait
+                                        (griddepcontrol.wait) for its completion and memory before
+                                        they read any input.  Stream order is fully kept. */
+#define TAGG_FLAG_PDL_OVERLAP 64u    /* the caller asserts that the kernel launched right before this
+                                        one in the stream writes none of this launch's inputs (A, S_A,
+                                        B, S_B, group sizes, c_row_offsets), e.g. a chain of independent
+                                        grouped GEMMs over resident operands.  Then the main loop runs
+                                        during the previous grid's tail and only the global stores
+                                        (C, tile map, error flag) wait for its completion, which keeps
+                                        write-after-write order on a shared C.  Ignored with SERIAL. */
 /* Cap the persistent grid at n SMs (flags bits 16-27; 0 = every SM).  An overlapped
    expert-parallel exchange leaves the rest to the NCCL kernels that run beside the GEMM. */
 #define TAGG_SM_LIMIT_SHIFT 16
@@ -111,6 +116,20 @@ int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa, int64_t m
                           int64_t c_rows, const int64_t* c_row_offsets, int32_t* tile_map,
                           uint32_t flags, void* stream);
 
+/*
+ * The same with a device error flag (nullable DEVICE int32, OR-ed, never cleared): the group
+ * sizes live on the device, so the kernel validates them.  Bit 0: a negative M_g (ConfigError,
+ * engine.py:82-92).  Bit 1: sum(M_g) > m_alloc, or more rows than C holds (c_rows without
+ * c_row_offsets; with them, a non-empty group's rows outside [0, c_rows)) (ShapeMismatch,
+ * engine.py:132-142).  A launch that flags does no loads, stores or tile-map writes at all.
+ */
+int tagg_grouped_gemm_fp8_checked(const void* a, int64_t lda, const float* sa, int64_t m_alloc,
+                                  const void* b, int b_layout, int b_experts, const float* sb,
+                                  int64_t sb_stride_g, int64_t sb_stride_kb, int64_t sb_stride_nb,
+                                  const int32_t* group_sizes, int G, int N, int K, void* c, int64_t ldc,
+                                  int64_t c_rows, const int64_t* c_row_offsets, int32_t* tile_map,
+                                  int32_t* err_flag, uint32_t flags, void* stream);
+
 /* Upper bound on the tile count, to size tile_map (no device data needed). */
 int64_t tagg_max_tiles(int64_t m_alloc, int G, int N);
 
@@ -145,8 +164,9 @@ int64_t tagg_padded_rows_bound(int64_t m_alloc, int G);
  *   dest_rows    DEVICE int32 [rows]         <- row of the padding-free grouped layout:
  *                experts in order, rows of one expert in ascending source order
  *   workspace    DEVICE int32 [tagg_route_workspace_ints(rows, num_experts)]
- * Out-of-range ids are skipped and flagged (tagg_route_error).  Stream-ordered,
- * no host sync.
+ * Out-of-range ids (e.g. -1 for a token the router dropped) get dest_rows = -1, are
+ * counted in no group and are flagged (tagg_route_error); the quantize / dispatch,
+ * combine and router-gradient kernels skip such routes.  Stream-ordered, no host sync.
  */
 int64_t tagg_route_workspace_ints(int64_t rows, int num_experts);
 int tagg_route_plan(const int32_t* expert_ids, int64_t rows, int num_experts, int32_t* group_sizes,
@@ -266,8 +286,8 @@ int tagg_swiglu_backward_quantize(const void* h, int64_t ldh, const void* dh, in
                                   int64_t lddgu, void* a, int64_t lda, float* sa, int32_t* err_flag, void* stream);
 /*
  * Top-k combine of the down GEMM output: out[t, :] = bf16( sum_{k < topk} fl(w[t,k] * c[dest[t*topk+k], :]) ),
- * accumulated in fp32 in k order with separate roundings (no FMA).  dest = the dispatch plan's
- * dest_rows (tagg_route_plan); c bf16 [rows, N] (pitch ldc), out bf16 [tokens, N] (pitch ldo),
+ * accumulated in fp32 in k order with separate roundings (no FMA); routes with dest < 0 (dropped)
+ * contribute nothing.  dest = the dispatch plan's dest_rows (tagg_route_plan); c bf16 [rows, N] (pitch ldc), out bf16 [tokens, N] (pitch ldo),
  * N % 8 == 0, topk <= 8, 16-byte aligned bases and pitches.
  */
 int tagg_combine(const void* c, int64_t ldc, const int32_t* dest_rows, const float* weights, int64_t tokens, int topk,

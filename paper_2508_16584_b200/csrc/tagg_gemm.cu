@@ -82,14 +82,16 @@ struct Params {
   const int32_t* group_sizes;
   const int64_t* c_row_offsets;
   int32_t* tile_map;
+  int32_t* err_flag;          // nullable DEVICE int32: |= 1 negative M_g, |= 2 rows past m_alloc / c_rows
   unsigned long long* trace;  // diagnostics: per-event clock64 stamps of CTAs 0/1 (tagg_debug_trace)
-  int64_t m_alloc;
+  int64_t m_alloc, c_rows;
   int64_t sb_sg, sb_skb, sb_snb;
   int32_t G, N, K, kb_count, n_tiles, sa_rb, b_kmajor, b_shared;
   uint32_t stages, sa_buf_bytes;
   uint32_t epi_passes;  // 256-column tiles: 1 = 64 KB staging, all 4 chunks at once; 2 = 32 KB, two passes
   uint32_t off_a, off_b, off_c, off_sa, off_sb, off_tab, off_bar;
   uint32_t dbg;
+  uint32_t pdl_overlap;  // TAGG_FLAG_PDL_OVERLAP: inputs are not written by the previous grid
 };
 
 template <int kCG, int kBN_>
@@ -262,12 +264,34 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<kCG>(tmem_slot, kTmemCols);
+  // Programmatic dependent launch.  By default every thread waits here for the previous grid
+  // in the stream (its completion and memory), so all inputs -- group sizes, A, S_A, B, S_B --
+  // are read after it: only the barrier init, the TMEM allocation and this grid's launch
+  // overlap the previous grid's tail.  With TAGG_FLAG_PDL_OVERLAP the caller asserts the
+  // previous grid writes none of this launch's inputs; then the main loop may overlap it and
+  // only the stores wait (WAW on C and the tile map, below).
+  if (!p.pdl_overlap) griddep_wait();
   if (warp == 2) {
-    // device-side prefix sums over M_g: row offsets and (pair-)tile offsets
+    // device-side prefix sums over M_g: row offsets and (pair-)tile offsets.  Sizes are
+    // validated here (they never reach the host): a negative M_g (ConfigError,
+    // engine.py:77-92) or more rows than A / C hold (ShapeMismatch, engine.py:132-142) sets
+    // *err_flag and the launch does no work at all (no load, store or tile-map write).
     int carry_r = 0, carry_t = 0;
+    long long rows64 = 0;
+    bool neg = false, oob = false;
     for (int base = 0; base < G; base += 32) {
       const int g = base + lane;
-      const int m = (g < G) ? max(0, p.group_sizes[g]) : 0;
+      const int graw = (g < G) ? p.group_sizes[g] : 0;
+      neg |= graw < 0;
+      const int m = max(0, graw);
+      if (g < G && p.c_row_offsets) {
+        const long long o = p.c_row_offsets[g];
+        oob |= m > 0 && (o < 0 || o + m > p.c_rows);
+      }
+      long long s64 = m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s64 += __shfl_xor_sync(0xffffffffu, s64, o);
+      rows64 += s64;
       const int tl = ((m + C::kTileM - 1) / C::kTileM) * p.n_tiles;
       int im = m, it = tl;
 #pragma unroll
@@ -285,16 +309,23 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       carry_r += __shfl_sync(0xffffffffu, im, 31);
       carry_t += __shfl_sync(0xffffffffu, it, 31);
     }
+    neg = __any_sync(0xffffffffu, neg);
+    oob = __any_sync(0xffffffffu, oob) || rows64 > p.m_alloc || (!p.c_row_offsets && rows64 > p.c_rows);
     if (lane == 0) {
       tab_row[G] = carry_r;
-      tab_tile[G] = carry_t;
+      tab_tile[G] = (neg || oob) ? 0 : carry_t;
+      if ((neg || oob) && p.err_flag && blockIdx.x == 0) {
+        griddep_wait();  // the flag is an output: after the previous grid, like every store
+        atomicOr(p.err_flag, (neg ? 1 : 0) | (oob ? 2 : 0));
+      }
     }
   }
   tc_fence_before();
   if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
-  // The next grouped GEMM in the stream (PDL launch) may start on SMs this grid releases;
-  // it only waits for this grid before its first global store (see griddep_wait below).
+  // The next grouped GEMM in the stream (PDL launch) may start on SMs this grid releases; it
+  // waits for this grid's completion before it reads its inputs (default) or, with
+  // TAGG_FLAG_PDL_OVERLAP, before its first global store.
   griddep_launch_dependents();
   // Values needed after the setmaxnreg split are re-read inside each role (ld.shared is
   // cheap); keeping them live across it makes ptxas spill them into the hot loops.
@@ -458,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
     uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0, tiles_done = 0;
-    bool prev_grid_done = false;
+    bool prev_grid_done = !p.pdl_overlap;  // default mode waited in the prologue
 #ifdef TAGG_TRACE
     const bool tr_a = p.trace != nullptr && pw == 0 && lane == 0;
     const bool tr_b = p.trace != nullptr && pw == 4 && lane == 0;
@@ -767,6 +798,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   }
 
   // ------------------------------------------------------------ teardown
+  // A grid that stored nothing (empty launch, or only empty tiles) still completes only after
+  // the previous grid: one wait per CTA keeps "grid i done => grid i-1 done" along the stream.
+  if (threadIdx.x == 0) griddep_wait();
   __syncwarp();
   tc_fence_before();
   if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
@@ -1020,6 +1054,17 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
                                      const int32_t* group_sizes, int G, int N, int K, void* c, int64_t ldc,
                                      int64_t c_rows, const int64_t* c_row_offsets, int32_t* tile_map,
                                      uint32_t flags, void* stream) {
+  return tagg_grouped_gemm_fp8_checked(a, lda, sa, m_alloc, b, b_layout, b_experts, sb, sb_stride_g, sb_stride_kb,
+                                       sb_stride_nb, group_sizes, G, N, K, c, ldc, c_rows, c_row_offsets, tile_map,
+                                       nullptr, flags, stream);
+}
+
+extern "C" int tagg_grouped_gemm_fp8_checked(const void* a, int64_t lda, const float* sa, int64_t m_alloc,
+                                             const void* b, int b_layout, int b_experts, const float* sb,
+                                             int64_t sb_stride_g, int64_t sb_stride_kb, int64_t sb_stride_nb,
+                                             const int32_t* group_sizes, int G, int N, int K, void* c,
+                                             int64_t ldc, int64_t c_rows, const int64_t* c_row_offsets,
+                                             int32_t* tile_map, int32_t* err_flag, uint32_t flags, void* stream) {
   // ---- ProblemConfig rules (engine.py:77-92) and operand checks (engine.py:132-142)
   if (K < 16 || K % 16 != 0) return TAGG_ERR_CONFIG;
   if (N < 64 || N % 64 != 0) return TAGG_ERR_CONFIG;
@@ -1061,8 +1106,10 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   p.group_sizes = group_sizes;
   p.c_row_offsets = c_row_offsets;
   p.tile_map = tile_map;
+  p.err_flag = err_flag;
   p.trace = g_trace;
   p.m_alloc = m_alloc;
+  p.c_rows = c_rows;
   p.sb_sg = sb_stride_g;
   p.sb_skb = sb_stride_kb;
   p.sb_snb = sb_stride_nb;
@@ -1142,6 +1189,7 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
   // PDL: this launch may start while the previous grid in the stream drains (it stores only
   // after that grid completed); TAGG_FLAG_SERIAL restores plain stream order
   const bool pdl = (flags & TAGG_FLAG_SERIAL) == 0;
+  p.pdl_overlap = (pdl && (flags & TAGG_FLAG_PDL_OVERLAP)) ? 1u : 0u;
   if (cg == 1) e = launch_cfg<1, 128>(p, smem_bytes, grid, st, exact, swz, pdl);
   else if (bn == 128) e = launch_cfg<2, 128>(p, smem_bytes, grid, st, exact, swz, pdl);
   else e = launch_cfg<2, 256>(p, smem_bytes, grid, st, exact, swz, pdl);

@@ -254,6 +254,10 @@ __global__ void __launch_bounds__(256) router_grad_kernel(const uint16_t* __rest
   const int lane = threadIdx.x & 31;
   const int64_t p = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (p >= pairs) return;
+  if (dest[p] < 0) {  // dropped route (tagg_route_plan wrote -1): no expert output, no gradient
+    if (lane == 0) g[p] = 0.0f;
+    return;
+  }
   const uint16_t* a = dy + (p / topk) * lddy;
   const uint16_t* b = c + static_cast<int64_t>(dest[p]) * ldc;
   float acc = 0.0f;
@@ -290,6 +294,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const uint16_t* __restrict
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
     for (int k = 0; k < topk; ++k) {
+      if (rows[k] < 0) continue;  // dropped route (tagg_route_plan wrote -1) contributes nothing
       const uint4 q = *reinterpret_cast<const uint4*>(c + static_cast<int64_t>(rows[k]) * ldc + 8 * c8);
       const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
       const float wk = ws[k];

@@ -140,6 +140,8 @@ __global__ void __launch_bounds__(32) route_rank_kernel(const int32_t* __restric
     if (ok && e >= 0) {
       dest[r] = pos;
       if (lane == leader) run[e] += __popc(same);
+    } else if (ok) {
+      dest[r] = -1;  // an id outside [0, E) (e.g. a router's -1 for a dropped token): no row
     }
     __syncwarp();
   }
@@ -245,6 +247,7 @@ __global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __re
       for (int k = 0; k < 8; ++k) {
         if (k >= topk) break;
         const int64_t row = d[k];
+        if (row < 0) continue;  // dropped / invalid route (route_rank_kernel wrote -1)
         if (full16) {
           *reinterpret_cast<uint4*>(a + row * lda + c0) = make_uint4(word[0], word[1], word[2], word[3]);
         } else {

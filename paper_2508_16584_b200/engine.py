@@ -33,6 +33,9 @@ FLAG_SINGLE_CTA = 4
 FLAG_TILE_N128 = 8
 FLAG_TILE_N256 = 16
 FLAG_SERIAL = 32  # no programmatic dependent launch (include/tagg.h TAGG_FLAG_SERIAL)
+FLAG_PDL_OVERLAP = 64  # inputs not written by the previous kernel: overlap its tail (TAGG_FLAG_PDL_OVERLAP)
+ERR_NEGATIVE_SIZE = 1  # device error flag bits (tagg_grouped_gemm_fp8_checked)
+ERR_ROWS_OUT_OF_RANGE = 2
 SM_LIMIT_SHIFT = 16  # TAGG_SM_LIMIT(n): cap the persistent grid at n SMs (include/tagg.h)
 TILES = {None: 0, "auto": 0, "1cta": FLAG_SINGLE_CTA, "pair_n128": FLAG_TILE_N128, "pair_n256": FLAG_TILE_N256}
 TILE_MAP_FIELDS = 9
@@ -153,6 +156,20 @@ class GroupedOperands:
             if dt not in (np.float32, torch.float32):
                 raise ShapeMismatch("scales must be float32")
 
+    @classmethod
+    def from_dense(cls, a, b, *, device="cuda") -> "GroupedOperands":
+        """engine.py:144-148: quantize dense A (1x128 tiles, fp8.py:132-151) and B (128x128
+        blocks, fp8.py:154-176; [K,N] shared or [G,K,N] per expert) -- on the GPU
+        (csrc/tagg_quant.cu, bit-identical to the reference), returning numpy codes and
+        scales as the reference does.  Non-finite entries raise InvalidInput (fp8.py:54-80)."""
+        from .quant import quantize_blocks, quantize_row_tiles
+
+        at = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+        bt = b if isinstance(b, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(b, dtype=np.float32))
+        ac, asc = quantize_row_tiles(at.to(device), check=True)
+        bc, bsc = quantize_blocks(bt.to(device), check=True)
+        return cls(ac.cpu().numpy(), asc.cpu().numpy(), bc.cpu().numpy(), bsc.cpu().numpy())
+
 
 def _to_dev_u8(x, device):
     x = _codes(x)
@@ -176,7 +193,7 @@ def _ptr(t):
 
 def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", out=None, c_row_offsets=None,
                      tile_map=None, exact_promotion=False, plain_staging=False, single_cta=False, tile=None,
-                     stream=None, max_sms=None, pdl=True):
+                     stream=None, max_sms=None, pdl=True, pdl_overlap=False, err_flag=None, check=False):
     """Padding-free FP8 grouped GEMM on device tensors (no host sync).
 
     a [m_alloc,K] uint8 / float8_e4m3fn; a_scales [m_alloc,ceil(K/128)] f32;
@@ -187,6 +204,18 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
     c_row_offsets[g].  ``tile`` picks the tile shape: "pair_n256" (CTA pair,
     256x256), "pair_n128" (CTA pair, 256x128), "1cta" (128x128) or None/"auto" (pair 256x256,
     or 1-CTA tiles when 3 G <= m_alloc <= 128 G: skinny, HBM-bound groups).
+
+    Group sizes never reach the host, so the kernel validates them: a negative M_g or
+    more rows than A / ``out`` hold makes the launch write nothing and OR-s a bit into
+    ``err_flag`` (an int32 CUDA tensor [1]; ERR_NEGATIVE_SIZE / ERR_ROWS_OUT_OF_RANGE).
+    ``check=True`` allocates the flag, synchronizes and raises ConfigError /
+    ShapeMismatch like the reference (engine.py:77-92, 132-142).
+
+    ``pdl`` (default on): programmatic dependent launch; the grid starts during the
+    previous kernel's tail but reads its inputs only after that kernel completed.
+    ``pdl_overlap=True`` asserts the previous kernel in the stream writes none of this
+    call's inputs (e.g. a chain of independent GEMMs over resident operands): the main
+    loop then overlaps it too, and only the stores wait (include/tagg.h).
     """
     if not (isinstance(a, torch.Tensor) and a.is_cuda):
         raise ValueError("grouped_gemm_fp8 expects CUDA tensors (no CPU fallback)")
@@ -232,23 +261,44 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
         raise ShapeMismatch("B must be contiguous")
     if out is None:
         out = torch.empty((m_alloc, N), dtype=torch.bfloat16, device=a.device)
-    if out.dtype not in (torch.bfloat16, torch.uint16, torch.int16) or out.stride(1) != 1:
+    if out.dtype not in (torch.bfloat16, torch.uint16, torch.int16) or out.stride(1) != 1 or out.dim() != 2:
         raise ShapeMismatch("out must be a row-major bf16 [c_rows, N] tensor")
+    if out.shape[1] != N:
+        raise ShapeMismatch(f"out has {out.shape[1]} columns, the problem has N={N}")
+    if c_row_offsets is None and out.shape[0] < m_alloc:
+        raise ShapeMismatch(f"out has {out.shape[0]} rows < m_alloc={m_alloc} (the rows of A)")
+    if out.device != a.device:
+        raise ShapeMismatch("out must be on the same device as A")
     if c_row_offsets is not None and (c_row_offsets.dtype != torch.int64 or not c_row_offsets.is_cuda):
         raise ShapeMismatch("c_row_offsets must be an int64 CUDA tensor")
     flags = ((FLAG_EXACT_PROMOTION if exact_promotion else 0) | (FLAG_PLAIN_C_STAGING if plain_staging else 0)
-             | (FLAG_SINGLE_CTA if single_cta else 0) | TILES[tile] | (0 if pdl else FLAG_SERIAL))
+             | (FLAG_SINGLE_CTA if single_cta else 0) | TILES[tile] | (0 if pdl else FLAG_SERIAL)
+             | (FLAG_PDL_OVERLAP if pdl_overlap else 0))
     if max_sms:
         if not 0 < int(max_sms) < 4096:
             raise ConfigError(f"max_sms must be in [1, 4095], got {max_sms}")
         flags |= int(max_sms) << SM_LIMIT_SHIFT
     st = stream if stream is not None else torch.cuda.current_stream(a.device)
-    rc = lib().tagg_grouped_gemm_fp8(
+    if check and err_flag is None:
+        err_flag = torch.zeros(1, dtype=torch.int32, device=a.device)
+    if err_flag is not None and (err_flag.dtype != torch.int32 or not err_flag.is_cuda):
+        raise ShapeMismatch("err_flag must be an int32 CUDA tensor")
+    rc = lib().tagg_grouped_gemm_fp8_checked(
         _ptr(a), a.stride(0), _ptr(a_scales), m_alloc, _ptr(b), layout, b_experts, _ptr(b_scales),
         sb_g, sb_kb, sb_nb, _ptr(group_sizes), G, N, K, _ptr(out), out.stride(0), out.shape[0],
-        _ptr(c_row_offsets), _ptr(tile_map), flags, st.cuda_stream)
+        _ptr(c_row_offsets), _ptr(tile_map), _ptr(err_flag), flags, st.cuda_stream)
     raise_for_status(rc, "tagg_grouped_gemm_fp8")
+    if check:
+        raise_for_device_flag(int(err_flag.item()), "tagg_grouped_gemm_fp8")
     return out
+
+
+def raise_for_device_flag(bits: int, what: str) -> None:
+    """The kernel's device-side validation of the group sizes (tagg_grouped_gemm_fp8_checked)."""
+    if bits & ERR_NEGATIVE_SIZE:
+        raise ConfigError(f"{what}: group sizes must be non-negative")
+    if bits & ERR_ROWS_OUT_OF_RANGE:
+        raise ShapeMismatch(f"{what}: sum of group sizes exceeds the rows of A / out")
 
 
 def max_tiles(m_alloc: int, groups: int, n: int) -> int:

@@ -79,8 +79,11 @@ def run_host_batches(batches, b: torch.Tensor, b_scales: torch.Tensor, *, b_layo
         m_alloc = a.shape[0]
         if sl["c"] is None or sl["c"].shape[0] < m_alloc or sl["c"].shape[1] != n:
             sl["c"] = torch.empty((max(m_alloc, 1), n), dtype=torch.bfloat16, device=dev)
+        # The only same-stream predecessor is the previous batch's GEMM, which writes another
+        # C slot (or, at depth 1, this one: the stores keep WAW order); the inputs arrive by
+        # event from the copy stream.  So the main loop may overlap that GEMM's tail.
         c = grouped_gemm_fp8(a, sa, b, b_scales, gs, b_layout=b_layout, out=sl["c"],
-                             exact_promotion=exact_promotion)
+                             exact_promotion=exact_promotion, pdl_overlap=True)
         sl["read"] = torch.cuda.Event()
         sl["read"].record(compute)
         rows = int(bt.group_sizes.sum()) if not bt.group_sizes.is_cuda else m_alloc

@@ -90,9 +90,19 @@ def wgrad_fp8(x_codes, x_scales, dy_codes, dy_scales, group_sizes, out=None) -> 
             raise ShapeMismatch("operands must be contiguous")
     if x_scales.shape[1] != k or dy_scales.shape[1] != n:
         raise ShapeMismatch("scales must be [TB, K] and [TB, N]")
+    if group_sizes.dtype != torch.int32 or not group_sizes.is_cuda:
+        raise ShapeMismatch("group_sizes must be an int32 CUDA tensor")
     g = group_sizes.numel()
+    tb = lib().tagg_token_blocks_bound(m, g)
+    if x_scales.dtype != torch.float32 or dy_scales.dtype != torch.float32:
+        raise ShapeMismatch("scales must be float32")
+    if x_scales.shape[0] < tb or dy_scales.shape[0] < tb:
+        raise ShapeMismatch(f"scales need >= {tb} token-block rows (tagg_token_blocks_bound)")
     if out is None:
         out = torch.empty((g, k, n), dtype=torch.bfloat16, device=x_codes.device)
+    if (out.dtype not in (torch.bfloat16, torch.int16, torch.uint16) or tuple(out.shape) != (g, k, n)
+            or not out.is_contiguous() or out.device != x_codes.device):
+        raise ShapeMismatch(f"out must be a contiguous bf16 [{g}, {k}, {n}] tensor on the operands' device")
     rc = lib().tagg_wgrad_fp8(x_codes.data_ptr(), x_scales.data_ptr(), dy_codes.data_ptr(), dy_scales.data_ptr(), m,
                               group_sizes.data_ptr(), g, k, n, out.data_ptr(), _stream())
     raise_for_status(rc, "tagg_wgrad_fp8")

@@ -198,3 +198,27 @@ def test_moe_oracle_combine_and_swiglu_against_float64():
     # bf16 RNE ties (engine.py:49 goldens, test_engine.py:49-62)
     assert list(omoe.bf16_rne(np.array([0x3F808000, 0x3F818000, 0x3F808001], np.uint32).view(np.float32))) == \
         [0x3F80, 0x3F82, 0x3F81]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_input_recipe_reproduces_golden_operand_bytes(name):
+    """oracle/fp8.random_operands (the restatement of cli.py:112-121 + fp8.py:54-176) draws
+    exactly the operand bytes the reference wrote for every fixture.  The GPU quantizer
+    tests compare against this restatement, so this pins it to the reference itself."""
+    c = load_case(name)
+    sizes, n, k, seed = c["group_sizes"], c["n"], c["k"], c["seed"]
+    m = int(sum(sizes))
+    ac, asc, bc, bsc = ofp8.random_operands(m, n, k, seed)
+    assert np.array_equal(ac, c["a_codes"]), "A codes"
+    assert np.array_equal(asc.view(np.uint32), c["a_scales"].view(np.uint32)), "A scales"
+    if c["b_layout"] == "shared_kn":
+        assert np.array_equal(bc, c["b_codes"]), "B codes"
+        assert np.array_equal(bsc.view(np.uint32), c["b_scales"].view(np.uint32)), "B scales"
+        return
+    # per-expert fixtures: expert g's B is drawn from seed * 1000 + 17 + g (make_golden.py)
+    for g in range(len(sizes)):
+        _, _, b, sb = ofp8.random_operands(1, n, k, seed * 1000 + 17 + g)
+        if c["b_layout"] == "expert_nk":
+            b, sb = b.T, sb.T
+        assert np.array_equal(b, c["b_codes"][g]), f"B codes expert {g}"
+        assert np.array_equal(sb.view(np.uint32), np.ascontiguousarray(c["b_scales"][g]).view(np.uint32)), g
