@@ -80,6 +80,43 @@ def deepseek_gateup_sizes(seed=0, tokens=32768, topk=8, experts=256, local=32, z
     return counts, counts[:local]
 
 
+def headline_operands(seed, m_alloc, n=4096, k=7168, experts=8):
+    """The headline's resident operands as numpy arrays, drawn from one seed, so the GPU arm
+    and the reference (CPU) arm compute on the very same bytes: uniform finite e4m3 codes
+    (no NaN code) and positive fp32 scales 2^[-12,-5) x [0.5, 1)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    kb, nb = -(-k // 128), -(-n // 128)
+
+    def codes(shape):
+        c = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        c[(c & 0x7F) == 0x7F] -= 1
+        return c
+
+    def scales(shape):
+        e = rng.integers(-12, -4, size=shape).astype(np.float32)
+        return ((rng.random(shape, dtype=np.float32) * np.float32(0.5) + np.float32(0.5)) * np.exp2(e)).astype(
+            np.float32)
+
+    return codes((m_alloc, k)), scales((m_alloc, kb)), codes((experts, k, n)), scales((experts, kb, nb))
+
+
+HEADLINE_SEED = 1000  # + rank: each rank owns its own experts
+SAMPLE_R = 64         # the CPU sample / self-check problem of the sweep: M_g = 128 g + 64
+
+
+def headline_config(world, exact):
+    """The headline's config dict; both arms print exactly this."""
+    return {
+        "workload": "residual sweep (BASELINE.json configs[1]): per rank 8 experts, M_g=128g+r, r=1..127 "
+                    "(127 grouped GEMMs per step), N=4096, K=7168, per-expert B [8,7168,4096]",
+        "N": 4096, "K": 7168, "groups": 8, "rows_per_step": sum(sum(s) for s in sweep_problems()),
+        "parallelism": f"ep{world} (experts sharded, no data-path collective)",
+        "l2": "inputs > L2: B is 235 MB per rank (126 MB L2), re-read from HBM every launch; no flush",
+        "promotion": "exact fmul+fadd" if exact else "ffma2",
+        "operands": f"bench.headline_operands(seed={HEADLINE_SEED}+rank): identical bytes in both arms",
+    }
+
+
 def _codes(torch, shape, gen, device):
     c = torch.randint(0, 256, shape, dtype=torch.uint8, device=device, generator=gen)
     return torch.where((c & 0x7F) == 0x7F, c - 1, c)  # never a NaN code
@@ -93,20 +130,23 @@ def _scales(torch, shape, gen, device):
 class Problem:
     """Resident device operands for one weight set and a list of group-size vectors."""
 
-    def __init__(self, torch, name, sizes_list, n, k, experts, device, seed, b_layout="kn"):
+    def __init__(self, torch, name, sizes_list, n, k, experts, device, seed, b_layout="kn", host=None):
         self.name, self.n, self.k, self.G = name, n, k, experts
         self.sizes_list = [tuple(int(x) for x in s) for s in sizes_list]
         self.m_alloc = max(sum(s) for s in self.sizes_list)
-        gen = torch.Generator(device=device).manual_seed(seed)
         kb, nb = -(-k // 128), -(-n // 128)
-        self.a = _codes(torch, (self.m_alloc, k), gen, device)
-        self.sa = _scales(torch, (self.m_alloc, kb), gen, device)
-        if b_layout == "kn":
-            self.b = _codes(torch, (experts, k, n), gen, device)
-            self.sb = _scales(torch, (experts, kb, nb), gen, device)
+        if host is not None:  # numpy operands (headline_operands), uploaded once
+            self.a, self.sa, self.b, self.sb = (torch.from_numpy(x).to(device) for x in host)
         else:
-            self.b = _codes(torch, (experts, n, k), gen, device)
-            self.sb = _scales(torch, (experts, nb, kb), gen, device)
+            gen = torch.Generator(device=device).manual_seed(seed)
+            self.a = _codes(torch, (self.m_alloc, k), gen, device)
+            self.sa = _scales(torch, (self.m_alloc, kb), gen, device)
+            if b_layout == "kn":
+                self.b = _codes(torch, (experts, k, n), gen, device)
+                self.sb = _scales(torch, (experts, kb, nb), gen, device)
+            else:
+                self.b = _codes(torch, (experts, n, k), gen, device)
+                self.sb = _scales(torch, (experts, nb, kb), gen, device)
         self.b_layout = b_layout
         self.gs = [torch.tensor(s, dtype=torch.int32, device=device) for s in self.sizes_list]
         self.out = torch.empty((self.m_alloc, n), dtype=torch.bfloat16, device=device)
@@ -225,21 +265,31 @@ def _flush_l2(torch, buf):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def cpu_sample(threads, target_s=10.0):
-    """Time the CPU oracle (C port of the reference's run_adaptive semantics)
-    on a bounded sample of the residual sweep: the r=64 problem (M_g = 128g+64,
-    8 experts, K=7168), restricted to a 128-aligned column slice whose width is
-    calibrated so the sample takes about target_s seconds."""
+def _parity(got_bits, want_bits):
+    """tests/helpers.REL_TOL: |c - c_ref| <= 2^-7 max(|c_ref|, 2^-10 rowabsmax(c_ref)) per element."""
+    got = (got_bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    ref = (want_bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    rowmax = np.abs(ref).max(axis=1, keepdims=True)
+    bad = np.abs(got - ref) > 2.0 ** -7 * np.maximum(np.abs(ref), 2.0 ** -10 * rowmax)
+    return {"out_of_tol": int(bad.sum()), "bit_identical": float((got_bits == want_bits).mean()),
+            "elements": int(ref.size)}
+
+
+def cpu_sample(threads, ops, target_s=10.0, got_bits=None):
+    """Time the CPU oracle (C port of the reference's run_adaptive semantics, every host
+    thread) on a bounded sample of the headline: the r=SAMPLE_R problem of the sweep
+    (M_g = 128 g + 64, 8 experts, K=7168) over the headline's own operands ``ops``
+    (headline_operands), on a 128-aligned column slice calibrated to ~target_s seconds.
+    With ``got_bits`` (the GPU arm's C of that problem, uint16 [m, 4096]) the sample is
+    also the parity check of the bench's own output: out-of-tolerance count and the
+    bit-identical fraction on the sampled columns."""
     from oracle import oracle as orc
 
-    sizes = tuple(128 * g + 64 for g in range(8))
-    n, k, G = 4096, 7168, 8
+    ac, asc, bc, bsc = ops
+    sizes = tuple(128 * g + SAMPLE_R for g in range(8))
+    n, k = bc.shape[-1], bc.shape[-2]
     m = sum(sizes)
-    rng = np.random.Generator(np.random.PCG64(1))
-    ac = rng.integers(0, 0x7E, size=(m, k), dtype=np.uint8)
-    asc = rng.uniform(0.5, 1.0, size=(m, k // 128)).astype(np.float32)
-    bc = rng.integers(0, 0x7E, size=(G, k, n), dtype=np.uint8)
-    bsc = rng.uniform(0.5, 1.0, size=(G, k // 128, n // 128)).astype(np.float32)
+    ac, asc = ac[:m], asc[:m]
     out = np.zeros((m, n), dtype=np.uint16)
     orc.grouped_gemm(ac, asc, bc, bsc, sizes, n_range=(0, 128), threads=threads, out=out)  # warm pages
     t0 = time.perf_counter()
@@ -250,32 +300,36 @@ def cpu_sample(threads, target_s=10.0):
     orc.grouped_gemm(ac, asc, bc, bsc, sizes, n_range=(0, cols), threads=threads, out=out)
     dt = time.perf_counter() - t0
     flops = 2.0 * m * cols * k
-    return flops / dt / 1e12, dt, f"residual sweep r=64 (M_g=128g+64, 8 experts, K=7168), N-slice [0,{cols}) of 4096: {flops:.3e} FLOP in {dt:.2f}s"
+    sample = (f"residual sweep r={SAMPLE_R} (M_g=128g+{SAMPLE_R}, 8 experts, K=7168) on the headline's operands, "
+              f"N-slice [0,{cols}) of {n}: {flops:.3e} FLOP in {dt:.2f}s")
+    par = None if got_bits is None else _parity(got_bits[:m, :cols], out[:, :cols])
+    return flops / dt / 1e12, dt, sample, par
 
 
 def reference_arm(args, rank, world):
-    """--impl reference: the reference's CPU implementation of the path (oracle
-    port, all host threads) on the same metric/config, rank 0 only."""
+    """--impl reference: the reference's CPU implementation of the path (oracle port, all
+    host threads) on the same metric, config and operands as the GPU arm, rank 0 only."""
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
     from oracle import oracle as orc  # noqa: F401  (built by __graft_entry__.build)
 
+    ops = headline_operands(HEADLINE_SEED, max(sum(s) for s in sweep_problems()))
     vals = []
     sample = ""
     # each step is a bounded sample of the headline workload (~5 s)
     for i in range(args.warmup + args.steps):
-        v, dt, sample = cpu_sample(threads, target_s=5.0 if i >= args.warmup else 1.0)
+        v, dt, sample, _ = cpu_sample(threads, ops, target_s=5.0 if i >= args.warmup else 1.0)
         if i >= args.warmup:
             vals.append((v, dt))
     value = statistics.median(v for v, _ in vals)
     ms = statistics.median(dt for _, dt in vals) * 1e3
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp8_e4m3 (fp32 accumulate)", "data": "synthetic",
-        "config": {"workload": "residual sweep (BASELINE.json configs[1]), CPU sample", "N": 4096, "K": 7168,
-                   "groups": 8},
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp8_e4m3 (fp32 accumulate, bf16 out)",
+        "data": "synthetic (uniform finite e4m3 codes, positive fp32 scales; per-rank expert weights)",
+        "config": headline_config(world, args.exact),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -291,7 +345,7 @@ def run_problem_set(torch, tg, prob, iters, warmup, flush=None, exact=False):
     def adaptive():
         for gs in prob.gs:
             tg.grouped_gemm_fp8(prob.a, prob.sa, prob.b, prob.sb, gs, b_layout=prob.b_layout, out=outs,
-                                exact_promotion=exact)
+                                exact_promotion=exact, pdl_overlap=True)
 
     def padded(unpad=True):
         for gs in prob.gs:
@@ -367,6 +421,47 @@ def measured_peak_deltas(torch, tg, prob, sizes):
     return out
 
 
+def _spawn(argv, gpus):
+    """--gpus N without a torchrun environment: run this script again under
+    torch.distributed.run, one rank per GPU (127.0.0.1 rendezvous), and return its status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve())] + argv
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank, world):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo): rank setup, the barrier-bracketed
+    timed region, the max over ranks and rank 0's single JSON line.  The step is a fixed
+    host workload, so the line carries no GEMM number ("dry_run": true)."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    x = np.random.default_rng(rank).standard_normal((256, 256)).astype(np.float32)
+    for _ in range(args.warmup):
+        x @ x
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x @ x
+    ms = (time.perf_counter() - t0) * 1e3
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    if rank == 0:
+        flops = world * args.steps * 2.0 * 256 ** 3
+        print(json.dumps({"metric": METRIC, "value": flops / (ms * 1e-3) / 1e12, "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dry_run": True,
+                          "config": headline_config(world, args.exact)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -379,11 +474,19 @@ def main():
     ap.add_argument("--ep1", action="store_true",
                     help="also run the DeepSeek-V3 down EP config (sequential vs overlapped) at one GPU")
     ap.add_argument("--profile-once", action="store_true", help="one step only (for ncu launch lists)")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing on CPU (gloo), no GPU work")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_spawn(sys.argv[1:], args.gpus))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        dry_run(args, rank, world)
+        return
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
@@ -402,42 +505,57 @@ def main():
 
     # ---------------------------------------------------------------- headline: residual sweep
     probs = sweep_problems()
-    P = Problem(torch, "residual_sweep", probs, 4096, 7168, 8, dev, seed=1000 + rank)
+    ops = headline_operands(HEADLINE_SEED + rank, max(sum(s) for s in probs))
+    P = Problem(torch, "residual_sweep", probs, 4096, 7168, 8, dev, seed=HEADLINE_SEED + rank, host=ops)
     flops_step = sum(P.flops)
     launches_per_step = len(probs)
 
-    def step():
-        for gs in P.gs:
-            tg.grouped_gemm_fp8(P.a, P.sa, P.b, P.sb, gs, out=P.out, exact_promotion=args.exact)
+    def make_step(exact):
+        def step():
+            # 127 independent GEMMs over resident operands: no launch writes the next one's
+            # inputs, so each may overlap its predecessor's tail (TAGG_FLAG_PDL_OVERLAP)
+            for gs in P.gs:
+                tg.grouped_gemm_fp8(P.a, P.sa, P.b, P.sb, gs, out=P.out, exact_promotion=exact, pdl_overlap=True)
+        return step
 
+    step = make_step(args.exact)
     if args.profile_once:
         step()
         torch.cuda.synchronize()
         return
 
-    # One step = 127 launches; it is captured once as a CUDA graph, so the timed
-    # region measures device work rather than per-launch host overhead.
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        with torch.cuda.graph(graph, stream=side):
-            step()
-    torch.cuda.current_stream().wait_stream(side)
+    def graph_of(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                fn()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        return graph
 
+    # The timed step is the 127 launches issued from the host (PDL chains them on the device);
+    # a CUDA-graph replay of the same launches is reported beside it (value_graph).
     with ClockSampler(local) as clk:  # sampled over warm-up + timed steps (100 ms period)
-        ms_total = _timed_steps(torch, dist, world, graph.replay, args.steps, args.warmup)
+        ms_total = _timed_steps(torch, dist, world, step, args.steps, args.warmup)
     clocks = clk.summary()
     ms_step = ms_total / args.steps
     value = world * flops_step / (ms_step * 1e-3) / 1e12
-    ms_eager = _timed_steps(torch, dist, world, step, max(2, args.steps // 2), 1) / max(2, args.steps // 2)
+    half = max(2, args.steps // 2)
+    g_main = graph_of(step)
+    ms_graph = _timed_steps(torch, dist, world, g_main.replay, half, 1) / half
+    del g_main
+    # the reference's own rounding order (engine.py:161-164: fl(acc + fl(inner * s))) timed as well
+    step_other = make_step(not args.exact)
+    ms_other = _timed_steps(torch, dist, world, step_other, half, 1) / half
 
     # ---------------------------------------------------------------- roofline (dominant kernel = the GEMM)
     launch_fns = [(lambda gs=gs: tg.grouped_gemm_fp8(P.a, P.sa, P.b, P.sb, gs, out=P.out,
-                                                     exact_promotion=args.exact)) for gs in P.gs]
+                                                     exact_promotion=args.exact, pdl_overlap=True)) for gs in P.gs]
     per_launch = _per_launch_ms(torch, launch_fns)
     achieved = sum(P.flops) / (sum(per_launch) * 1e-3) / 1e12
     traffic = None
@@ -447,42 +565,47 @@ def main():
     alg_bytes = sum(P.algorithmic_bytes(s) for s in P.sizes_list) / len(P.sizes_list)
 
     # ---------------------------------------------------------------- padded baseline, same GPU
-    base_tf, base_ms, ws_bytes = run_problem_set(torch, tg, P, iters=max(2, args.steps // 2), warmup=1,
-                                                 exact=args.exact)
+    base_tf, base_ms, ws_bytes = run_problem_set(torch, tg, P, iters=half, warmup=1, exact=args.exact)
     mem_measured = measured_peak_deltas(torch, tg, P, P.sizes_list[0])
     per_r = per_residue_speedups(torch, tg, P)
     acc = [tg.account(s, 4096, 7168) for s in P.sizes_list]
     saved_pct = 100.0 * (1 - sum(a.bytes_actual for a in acc) / sum(a.bytes_padded for a in acc))
 
     # ---------------------------------------------------------------- e2e through the public API
+    # Every one of the 127 problems is an independent host-buffer call: its own A rows, A scales
+    # and group sizes H2D from pinned memory, its C rows D2H; expert weights stay resident, as
+    # model parameters do.  hostpipe overlaps problem i's D2H and i+1's H2D with the GEMMs.
+    from paper_2508_16584_b200.hostpipe import HostBatch, run_host_batches
+
     pin_a = P.a.cpu().pin_memory()
     pin_sa = P.sa.cpu().pin_memory()
     pin_gs = [g.cpu().pin_memory() for g in P.gs]
     host_c = torch.empty((P.m_alloc, P.n), dtype=torch.bfloat16).pin_memory()
-    a_dev = torch.empty_like(P.a)
-    sa_dev = torch.empty_like(P.sa)
-    h2d = pin_a.numel() + pin_sa.numel() * 4 + sum(g.numel() * 4 for g in pin_gs)
-    d2h = sum(sum(s) * P.n * 2 for s in P.sizes_list)
-
-    from paper_2508_16584_b200.hostpipe import HostBatch, run_host_batches
+    rows = [sum(s) for s in P.sizes_list]
+    batches = [HostBatch(pin_a[:m], pin_sa[:m], gh, host_c) for m, gh in zip(rows, pin_gs)]
+    h2d = sum(m * (P.k + 4 * (P.k // 128)) + g.numel() * 4 for m, g in zip(rows, pin_gs))
+    d2h = sum(m * P.n * 2 for m in rows)
 
     def e2e_step():
-        # A and S_A once per step; then the 127 GEMMs with each one's group sizes H2D and its
-        # C rows D2H overlapped with the next GEMMs (hostpipe.run_host_batches)
-        a_dev.copy_(pin_a, non_blocking=True)
-        sa_dev.copy_(pin_sa, non_blocking=True)
-        run_host_batches([HostBatch(a_dev, sa_dev, gh, host_c) for gh in pin_gs], P.b, P.sb,
-                         exact_promotion=args.exact)
+        run_host_batches(batches, P.b, P.sb, exact_promotion=args.exact)
 
-    e2e_ms = _timed_steps(torch, dist, world, e2e_step, max(2, args.steps // 2), 1) / max(2, args.steps // 2)
+    e2e_ms = _timed_steps(torch, dist, world, e2e_step, half, 1) / half
     e2e_val = world * flops_step / (e2e_ms * 1e-3) / 1e12
 
-    # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
+    # ---------------------------------------------------------------- CPU baseline + self-check (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        sizes = tuple(128 * g + SAMPLE_R for g in range(8))
+        c_chk = torch.empty((sum(sizes), P.n), dtype=torch.bfloat16, device=dev)
+        tg.grouped_gemm_fp8(P.a, P.sa, P.b, P.sb, torch.tensor(sizes, dtype=torch.int32, device=dev), out=c_chk,
+                            exact_promotion=args.exact)
+        got = c_chk.view(torch.int16).cpu().numpy().view(np.uint16)
         threads = len(os.sched_getaffinity(0))
-        v, dt, sample = cpu_sample(threads, target_s=10.0)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+        v, dt, sample, par = cpu_sample(threads, ops, target_s=10.0, got_bits=got)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+               "parity_vs_gpu_output": dict(par, tolerance="|c-c_ref| <= 2^-7 max(|c_ref|, 2^-10 rowabsmax)",
+                                            what=f"this run's GPU C of the r={SAMPLE_R} problem vs the CPU "
+                                                 "oracle on the same operands and columns")}
 
     # ---------------------------------------------------------------- other BASELINE configs
     # secondary lines never cost the headline: a failure is recorded, not raised
@@ -506,6 +629,8 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
+    cfg = headline_config(world, args.exact)  # identical to the reference arm's config
+    other = "value_ffma2" if args.exact else "value_exact"
     line = {
         "metric": METRIC,
         "value": value,
@@ -519,16 +644,11 @@ def main():
         "vs_baseline": None,
         "dtype": "fp8_e4m3 (fp32 accumulate, bf16 out)",
         "data": "synthetic (uniform finite e4m3 codes, positive fp32 scales; per-rank expert weights)",
-        "config": {
-            "workload": "residual sweep (BASELINE.json configs[1]): per rank 8 experts, M_g=128g+r, r=1..127 "
-                        "(127 grouped GEMMs per step), N=4096, K=7168, per-expert B [8,7168,4096]",
-            "N": 4096, "K": 7168, "groups": 8, "rows_per_step": sum(sum(s) for s in probs),
-            "parallelism": f"ep{world} (experts sharded, no data-path collective)",
-            "l2": "inputs > L2: B is 235 MB per rank (126 MB L2), re-read from HBM every launch; no flush",
-            "promotion": "exact fmul+fadd" if args.exact else "ffma2",
-            "launch": "timed step = replay of a CUDA graph of the 127 launches (value_eager: plain launches)",
-        },
-        "value_eager": world * flops_step / (ms_eager * 1e-3) / 1e12,
+        "config": cfg,
+        "timing": ("timed step = the 127 launches issued eagerly (programmatic dependent launch chains them); "
+                   "value_graph: the same launches replayed from a CUDA graph"),
+        "value_graph": world * flops_step / (ms_graph * 1e-3) / 1e12,
+        other: world * flops_step / (ms_other * 1e-3) / 1e12,
         "speedup_vs_padded": base_ms["padded"] / base_ms["adaptive"],
         "speedup_vs_padded_no_unpad": base_ms["padded_no_unpad"] / base_ms["adaptive"],
         "padded_baseline": {"value": base_tf["padded"], "value_no_unpad": base_tf["padded_no_unpad"], "unit": UNIT,
@@ -545,14 +665,55 @@ def main():
                      "traffic_source": "profiles/traffic_residual_sweep.json (ncu launch list, mean per launch)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "note": "A, S_A, group sizes H2D from pinned memory and every C D2H each step; expert weights resident; D2H of batch r overlaps the GEMMs after it (hostpipe.run_host_batches)"},
+                "note": "127 independent host-buffer calls per step: each copies its own A rows, A scales and group "
+                        "sizes H2D (pinned) and its C rows D2H; expert weights resident; copies overlap the GEMMs "
+                        "(hostpipe.run_host_batches)"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
         "extra": extra,
     }
+    line["summary"] = summarize(line, fp8_peak)
     print(json.dumps(line), flush=True)
+    print(line["summary"], file=sys.stderr, flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def summarize(line, fp8_peak):
+    """<= 1 KB of the numbers that matter, for the stdout / stderr tails the driver keeps."""
+    f = lambda x, d=0: "-" if x is None else f"{x:.{d}f}"  # noqa: E731
+    out = [f"headline {f(line['value'])} TF/s ({f(100 * line['value'] / line['n_gpus'] / fp8_peak, 1)}% of "
+           f"{fp8_peak:.0f}), graph {f(line.get('value_graph'))}, exact {f(line.get('value_exact'))}, "
+           f"vs padded {f(line['speedup_vs_padded'], 2)}x (per-r min {f(line['speedup_vs_padded_per_r']['min'], 2)}x), "
+           f"e2e {f(line['e2e']['value'])}, roofline {f(line['roofline']['frac'], 3)}"]
+    cpu = line.get("cpu_baseline")
+    if cpu:
+        p = cpu.get("parity_vs_gpu_output") or {}
+        out.append(f"cpu {f(cpu['value'], 3)} TF/s on {cpu['cores']} cores; self-check out_of_tol="
+                   f"{p.get('out_of_tol')} bit_identical={f(p.get('bit_identical'), 4)}")
+    ex = line.get("extra") or {}
+    short = {"deepseek_v3_gateup_ep8_rank0": "DSv3 gu", "deepseek_v3_down_256e_1gpu": "DSv3 down",
+             "qwen3_fwd_gateup": "Q3 fgu", "qwen3_fwd_down": "Q3 fdn", "qwen3_dgrad_down": "Q3 ddn",
+             "qwen3_dgrad_gateup": "Q3 dgu"}
+    cfgs = [f"{short[k]} {f(v['tflops'])} {f(100 * v['fp8_peak_frac'], 1)}% {f(v['speedup_vs_padded'], 2)}x"
+            for k, v in ex.items() if k in short and isinstance(v, dict) and "tflops" in v]
+    if cfgs:
+        out.append("; ".join(cfgs))
+    sk = (ex.get("skinny_sweep") or {}).get("per_r")
+    if sk:
+        out.append("skinny " + " ".join(f"r{d['r']}:{f(d['us'], 1)}us/{f(100 * d['hbm_frac'])}%/"
+                                        f"{f(d['speedup_vs_padded'], 2)}x" for d in sk))
+    for k, lab in (("wgrad_dsv3_gateup", "wgrad"), ("moe_ffn_dsv3_1gpu", "moe fwd")):
+        v = ex.get(k)
+        if isinstance(v, dict) and "tflops" in v:
+            out.append(f"{lab} {f(v['tflops'])} TF/s {f(100 * v['fp8_peak_frac'], 1)}%")
+    q = ex.get("quantize_dispatch_dsv3")
+    if isinstance(q, dict) and "gbs" in q:
+        out.append(f"quant+dispatch {f(q['gbs'])} GB/s {f(100 * q['hbm_frac'])}%")
+    ep = ex.get("deepseek_v3_down_ep")
+    if isinstance(ep, dict) and "gemm_tflops_aggregate" in ep:
+        out.append(f"ep{ep['world']} gemm {f(ep['gemm_tflops_aggregate'])} TF/s e2e {f(ep['e2e_tflops_aggregate_incl_a2a'])}")
+    return " | ".join(out)[:1024]
 
 
 def run_extra(torch, tg, dev, rank, fp8_peak, exact):
