@@ -265,8 +265,6 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
         raise ShapeMismatch("out must be a row-major bf16 [c_rows, N] tensor")
     if out.shape[1] != N:
         raise ShapeMismatch(f"out has {out.shape[1]} columns, the problem has N={N}")
-    if c_row_offsets is None and out.shape[0] < m_alloc:
-        raise ShapeMismatch(f"out has {out.shape[0]} rows < m_alloc={m_alloc} (the rows of A)")
     if out.device != a.device:
         raise ShapeMismatch("out must be on the same device as A")
     if c_row_offsets is not None and (c_row_offsets.dtype != torch.int64 or not c_row_offsets.is_cuda):
@@ -348,6 +346,7 @@ def padded_grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, ws: PaddedWor
     full-height store.  K3 optionally gathers the valid rows.  This is
     engine.py:346-402's data path.
     """
+    kw.pop("pdl_overlap", None)  # the pad kernel right before writes this GEMM's inputs
     pad_groups(a, a_scales, group_sizes, ws, stream)
     grouped_gemm_fp8(ws.a_pad, ws.sa_pad, b, b_scales, ws.padded_sizes, b_layout=b_layout, out=ws.c_pad,
                      stream=stream, **kw)
