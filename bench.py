@@ -980,7 +980,7 @@ def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, war
     state = {}
 
     def dispatch():
-        state["a"], state["sa"], state["meta"] = ep.dispatch(a, sa, eid, E)
+        state["a"], state["sa"], state["meta"] = ep.dispatch(a, sa, eid, E, in_place=True)
 
     def gemm():
         m = state["a"].shape[0]
@@ -988,7 +988,7 @@ def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, war
             state["out"] = torch.empty((max(m, 1), N), dtype=torch.bfloat16, device=dev)
         if m:
             tg.grouped_gemm_fp8(state["a"], state["sa"], b, sb, state["meta"].group_sizes, out=state["out"],
-                                exact_promotion=exact)
+                                exact_promotion=exact, b_index=state["meta"].b_index)
 
     def combine():
         m = state["a"].shape[0]
@@ -998,8 +998,9 @@ def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, war
     gemm_sms = sms - 16  # the overlapped path leaves 16 SMs to the NCCL kernels
     chunks = 4
 
-    def capped(codes, scales, gs):
-        return tg.grouped_gemm_fp8(codes, scales, b, sb, gs, exact_promotion=exact, max_sms=gemm_sms)
+    def capped(codes, scales, gs, b_index=None, out=None):
+        return tg.grouped_gemm_fp8(codes, scales, b, sb, gs, exact_promotion=exact, max_sms=gemm_sms,
+                                   b_index=b_index, out=out)
 
     def overlapped():
         state["ov"] = ep.pipelined_expert_gemm(a, sa, eid, E, capped, N, chunks=chunks)

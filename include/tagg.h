@@ -59,7 +59,7 @@ extern "C" {
                                         in the last wave of small problems) */
 #define TAGG_FLAG_TILE_N256 16u      /* CTA-pair tile 256x256.  With none of SINGLE_CTA / TILE_N128 /
                                         TILE_N256 set, the launch picks 256x256 pair tiles, or 1-CTA
-                                        128x128 tiles when 3 G <= m_alloc <= 128 G (HBM-bound skinny
+                                        128x128 tiles when m_alloc <= 128 G (HBM-bound skinny
                                         groups) */
 #define TAGG_FLAG_SERIAL 32u         /* no programmatic dependent launch.  By default a grouped GEMM
                                         is launched with PDL: when the previous kernel in the stream
@@ -117,18 +117,24 @@ int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa, int64_t m
                           uint32_t flags, void* stream);
 
 /*
- * The same with a device error flag (nullable DEVICE int32, OR-ed, never cleared): the group
- * sizes live on the device, so the kernel validates them.  Bit 0: a negative M_g (ConfigError,
- * engine.py:82-92).  Bit 1: sum(M_g) > m_alloc, or more rows than C holds (c_rows without
- * c_row_offsets; with them, a non-empty group's rows outside [0, c_rows)) (ShapeMismatch,
- * engine.py:132-142).  A launch that flags does no loads, stores or tile-map writes at all.
+ * The general entry point; tagg_grouped_gemm_fp8 is this with b_index = err_flag = NULL.
+ *  b_index   nullable DEVICE int32 [G]: group g multiplies B expert b_index[g] (0 <= . < b_experts),
+ *            so several groups may share one expert's weights -- e.g. the (source rank, expert)
+ *            segments an expert-parallel all-to-all delivers, read in place without a regroup.
+ *            NULL = group g uses expert g (b_experts == G) or the shared B (b_experts == 1).
+ *  err_flag  nullable DEVICE int32, OR-ed, never cleared.  The group sizes live on the device, so
+ *            the kernel validates them: bit 0 a negative M_g (ConfigError, engine.py:82-92); bit 1
+ *            sum(M_g) > m_alloc, or more rows than C holds (c_rows without c_row_offsets; with
+ *            them, a non-empty group's rows outside [0, c_rows)) (ShapeMismatch,
+ *            engine.py:132-142); bit 2 a non-empty group's b_index outside [0, b_experts).  A
+ *            launch that flags does no loads, stores or tile-map writes at all.
  */
-int tagg_grouped_gemm_fp8_checked(const void* a, int64_t lda, const float* sa, int64_t m_alloc,
-                                  const void* b, int b_layout, int b_experts, const float* sb,
-                                  int64_t sb_stride_g, int64_t sb_stride_kb, int64_t sb_stride_nb,
-                                  const int32_t* group_sizes, int G, int N, int K, void* c, int64_t ldc,
-                                  int64_t c_rows, const int64_t* c_row_offsets, int32_t* tile_map,
-                                  int32_t* err_flag, uint32_t flags, void* stream);
+int tagg_grouped_gemm_fp8_ex(const void* a, int64_t lda, const float* sa, int64_t m_alloc, const void* b,
+                             int b_layout, int b_experts, const float* sb, int64_t sb_stride_g,
+                             int64_t sb_stride_kb, int64_t sb_stride_nb, const int32_t* group_sizes, int G, int N,
+                             int K, void* c, int64_t ldc, int64_t c_rows, const int64_t* c_row_offsets,
+                             int32_t* tile_map, const int32_t* b_index, int32_t* err_flag, uint32_t flags,
+                             void* stream);
 
 /* Upper bound on the tile count, to size tile_map (no device data needed). */
 int64_t tagg_max_tiles(int64_t m_alloc, int G, int N);

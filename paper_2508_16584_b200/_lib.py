@@ -24,9 +24,9 @@ SIGNATURES = {
     "tagg_grouped_gemm_fp8": (c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_vp, c_i64, c_i64,
                                       c_i64, c_vp, c_int, c_int, c_int, c_vp, c_i64, c_i64, c_vp, c_vp,
                                       c_u32, c_vp]),
-    "tagg_grouped_gemm_fp8_checked": (c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_vp, c_i64, c_i64,
-                                              c_i64, c_vp, c_int, c_int, c_int, c_vp, c_i64, c_i64, c_vp, c_vp,
-                                              c_vp, c_u32, c_vp]),
+    "tagg_grouped_gemm_fp8_ex": (c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_int, c_int, c_vp, c_i64, c_i64,
+                                         c_i64, c_vp, c_int, c_int, c_int, c_vp, c_i64, c_i64, c_vp, c_vp,
+                                         c_vp, c_vp, c_u32, c_vp]),
     "tagg_max_tiles": (c_i64, [c_i64, c_int, c_int]),
     "tagg_launch_clusters": (c_int, [c_i64, c_int, c_int, c_u32]),
     "tagg_pad_groups": (c_int, [c_vp, c_i64, c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_i64, c_vp]),

@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -81,17 +82,21 @@ struct Params {
   const float* sb;
   const int32_t* group_sizes;
   const int64_t* c_row_offsets;
+  const int32_t* b_index;     // nullable DEVICE int32 [G]: group g multiplies B expert b_index[g]
   int32_t* tile_map;
   int32_t* err_flag;          // nullable DEVICE int32: |= 1 negative M_g, |= 2 rows past m_alloc / c_rows
   unsigned long long* trace;  // diagnostics: per-event clock64 stamps of CTAs 0/1 (tagg_debug_trace)
   int64_t m_alloc, c_rows;
   int64_t sb_sg, sb_skb, sb_snb;
-  int32_t G, N, K, kb_count, n_tiles, sa_rb, b_kmajor, b_shared;
+  int32_t G, N, K, kb_count, n_tiles, sa_rb, b_kmajor, b_shared, b_experts;
   uint32_t stages, sa_buf_bytes;
   uint32_t epi_passes;  // 256-column tiles: 1 = 64 KB staging, all 4 chunks at once; 2 = 32 KB, two passes
   uint32_t off_a, off_b, off_c, off_sa, off_sb, off_tab, off_bar;
   uint32_t dbg;
   uint32_t pdl_overlap;  // TAGG_FLAG_PDL_OVERLAP: inputs are not written by the previous grid
+  uint64_t l2_a, l2_b;   // L2 eviction policies of the A / B tile loads (0 = no hint)
+  float one;             // 1.0f (kExact promotion: an FFMA2 by a 1.0 the compiler cannot see)
+  uint32_t stage_tx;     // bytes landing per pipeline stage (both CTAs): A box rows x 128 + B box
 };
 
 template <int kCG, int kBN_>
@@ -208,6 +213,21 @@ __device__ __forceinline__ int sa_row_prev(int64_t row0, int rb) {
   return rp;
 }
 
+// The persistent grid's cluster count, re-read from %nctaid per use: kept live across the
+// tile loops in the 72-register control warps it was spilled to local memory.
+template <int kCG>
+__device__ __forceinline__ int grid_clusters() {
+  uint32_t n;
+  asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(n));
+  return static_cast<int>(n) / kCG;
+}
+template <int kCG>
+__device__ __forceinline__ int cluster_index() {
+  uint32_t c;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(c));
+  return static_cast<int>(c) / kCG;
+}
+
 template <int kCG, int kBN, bool kExact, bool kSwizzleC>
 __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_constant__ Params p) {
   using C = Cfg<kCG, kBN>;
@@ -219,8 +239,6 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   const int G = p.G;
   const int rank = (kCG == 2) ? static_cast<int>(cluster_ctarank()) : 0;
   const bool is_leader = rank == 0;
-  const int cluster_id = blockIdx.x / kCG;
-  const int num_clusters = gridDim.x / kCG;
 #ifdef TAGG_TRACE
   const uint32_t dbg = p.dbg;  // ablation switches exist only in the diagnostics build
 #else
@@ -236,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   int32_t* tab_row = tab_tile + (G + 1);                                // [G+1]
   int32_t* tab_size = tab_row + (G + 1);                                // [G]
   int32_t* tab_crow = tab_size + G;                                     // [G]
+  int32_t* tab_bidx = tab_crow + G;                                     // [G] B expert of group g
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
@@ -278,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     // *err_flag and the launch does no work at all (no load, store or tile-map write).
     int carry_r = 0, carry_t = 0;
     long long rows64 = 0;
-    bool neg = false, oob = false;
+    bool neg = false, oob = false, bad_b = false;
     for (int base = 0; base < G; base += 32) {
       const int g = base + lane;
       const int graw = (g < G) ? p.group_sizes[g] : 0;
@@ -287,6 +306,11 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       if (g < G && p.c_row_offsets) {
         const long long o = p.c_row_offsets[g];
         oob |= m > 0 && (o < 0 || o + m > p.c_rows);
+      }
+      if (g < G) {
+        const int bi = p.b_index ? p.b_index[g] : g;
+        bad_b |= m > 0 && !p.b_shared && (bi < 0 || bi >= p.b_experts);
+        tab_bidx[g] = p.b_shared ? 0 : bi;
       }
       long long s64 = m;
 #pragma unroll
@@ -310,13 +334,15 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       carry_t += __shfl_sync(0xffffffffu, it, 31);
     }
     neg = __any_sync(0xffffffffu, neg);
+    bad_b = __any_sync(0xffffffffu, bad_b);
     oob = __any_sync(0xffffffffu, oob) || rows64 > p.m_alloc || (!p.c_row_offsets && rows64 > p.c_rows);
     if (lane == 0) {
+      const bool bad = neg || oob || bad_b;
       tab_row[G] = carry_r;
-      tab_tile[G] = (neg || oob) ? 0 : carry_t;
-      if ((neg || oob) && p.err_flag && blockIdx.x == 0) {
+      tab_tile[G] = bad ? 0 : carry_t;
+      if (bad && p.err_flag && blockIdx.x == 0) {
         griddep_wait();  // the flag is an output: after the previous grid, like every store
-        atomicOr(p.err_flag, (neg ? 1 : 0) | (oob ? 2 : 0));
+        atomicOr(p.err_flag, (neg ? 1 : 0) | (oob ? 2 : 0) | (bad_b ? 4 : 0));
       }
     }
   }
@@ -345,10 +371,10 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
     const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
-    const int xs = tail_split_count(total_tiles, num_clusters, C::kHalfTiles);
-    for (int t = cluster_id; t < total_tiles + xs; t += num_clusters) {
+    const int xs = tail_split_count(total_tiles, grid_clusters<kCG>(), C::kHalfTiles);
+    for (int t = cluster_index<kCG>(); t < total_tiles + xs; t += grid_clusters<kCG>()) {
       const Tile T = decode_unit<kCG, kBN>(t, total_tiles, xs, rank, tab_tile, tab_row, tab_size, tab_crow, G);
-      const int gb = p.b_shared ? 0 : T.g;
+      const int gb = ld_shared_s32(smem_u32(&tab_bidx[T.g]));
       mbar_wait_addr(sempty0 + 8 * sab, saph ^ 1);
       // ---- S_B columns of the tile (engine.py:166-169: column block n // 128)
       {
@@ -396,11 +422,17 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             if (dbg & kDbgNoLoad) {
               if (is_leader) mbar_arrive_addr(fb);
             } else {
-              if (is_leader) mbar_arrive_expect_tx_addr(fb, C::kStageTx);
+              if (is_leader) mbar_arrive_expect_tx_addr(fb, p.stage_tx);
               const int cb0 = p.b_kmajor ? kb * BK : nb;
               const int cb1 = p.b_kmajor ? nb : kb * BK;
-              tma_load_2d_u32<kCG>(&p.tmap_a, fb, sA0 + stage * kStageBytesA, kb * BK, T.row0);
-              tma_load_3d_u32<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb);
+              if (p.l2_a)
+                tma_load_2d_hint<kCG>(&p.tmap_a, fb, sA0 + stage * kStageBytesA, kb * BK, T.row0, p.l2_a);
+              else
+                tma_load_2d_u32<kCG>(&p.tmap_a, fb, sA0 + stage * kStageBytesA, kb * BK, T.row0);
+              if (p.l2_b)
+                tma_load_3d_hint<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb, p.l2_b);
+              else
+                tma_load_3d_u32<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb);
             }
           }
           __syncwarp();
@@ -438,8 +470,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
       const uint32_t tfull0 = smem_u32(&tfull[0]), tempty0 = smem_u32(&tempty[0]);
       uint32_t stage = 0, phase = 0, acc = 0, accph = 0, kiter = 0;
-      const int xs = tail_split_count(total_tiles, num_clusters, C::kHalfTiles);
-      for (int t = cluster_id; t < total_tiles + xs; t += num_clusters) {
+      const int xs = tail_split_count(total_tiles, grid_clusters<kCG>(), C::kHalfTiles);
+      for (int t = cluster_index<kCG>(); t < total_tiles + xs; t += grid_clusters<kCG>()) {
         const uint32_t idesc_t =
             (C::kHalfTiles && decode_unit<kCG, kBN>(t, total_tiles, xs, 0, tab_tile, tab_row, tab_size, tab_crow, G).half)
                 ? idesc_half
@@ -488,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t tfull0 = opaque_u32(smem_u32(&tfull[0])), tempty0 = opaque_u32(smem_u32(&tempty[0]));
     const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
+    const float one = p.one;  // 1.0f from the launch parameters: ptxas cannot fold it
     uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0, tiles_done = 0;
     bool prev_grid_done = !p.pdl_overlap;  // default mode waited in the prologue
 #ifdef TAGG_TRACE
@@ -496,8 +529,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
 #else
     constexpr bool tr_a = false, tr_b = false;
 #endif
-    const int xs = tail_split_count(total_tiles, num_clusters, C::kHalfTiles);
-    for (int t = cluster_id; t < total_tiles + xs; t += num_clusters) {
+    const int xs = tail_split_count(total_tiles, grid_clusters<kCG>(), C::kHalfTiles);
+    for (int t = cluster_index<kCG>(); t < total_tiles + xs; t += grid_clusters<kCG>()) {
       const Tile T = decode_unit<kCG, kBN>(t, total_tiles, xs, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int rp = sa_row_prev(T.row0, rb);
       if (C::kHalfTiles && T.half) {
@@ -532,8 +565,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             }
             if constexpr (kExact) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                hacc[32 * c + i] = __fadd_rn(hacc[32 * c + i], __fmul_rn(__uint_as_float(v[i]), s));
+              for (int i = 0; i < 32; i += 2)
+                fma2_two_roundings(hacc[32 * c + i], hacc[32 * c + i + 1], __uint_as_float(v[i]),
+                                   __uint_as_float(v[i + 1]), s, one);
             } else {
 #pragma unroll
               for (int i = 0; i < 32; i += 2)
@@ -651,8 +685,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             acc[64 * c] += __uint_as_float(v[c]);
           } else if constexpr (kExact) {
 #pragma unroll
-            for (int i = 0; i < 64; ++i)
-              acc[64 * c + i] = __fadd_rn(acc[64 * c + i], __fmul_rn(__uint_as_float(v[i]), s));
+            for (int i = 0; i < 64; i += 2)
+              fma2_two_roundings(acc[64 * c + i], acc[64 * c + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                 s, one);
           } else {
 #pragma unroll
             for (int i = 0; i < 64; i += 2)
@@ -940,7 +975,7 @@ static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_a
   p.off_sa = p.off_c + staging_bytes;
   p.off_sb = p.off_sa + 2 * sa_buf;
   p.off_tab = p.off_sb + 2 * kSbBufBytes;
-  const uint32_t tab_bytes = align_up(4u * static_cast<uint32_t>(2 * (G + 1) + 2 * G), 16);
+  const uint32_t tab_bytes = align_up(4u * static_cast<uint32_t>(2 * (G + 1) + 3 * G), 16);
   p.off_bar = p.off_tab + tab_bytes;
   const uint32_t bar_bytes = (2 * stages + 2 * num_acc + 4) * 8 + 16;
   return p.off_bar + bar_bytes + 1024;
@@ -1021,15 +1056,16 @@ static int launch_sms(uint32_t flags, int cg) {
 }
 
 // Tile shape without an explicit TAGG_FLAG_SINGLE_CTA / _TILE_N128 / _TILE_N256: the CTA-pair
-// 256x256 tile, unless the groups average 3..128 rows (3 G <= m_alloc <= 128 G).  Such
-// launches are HBM-bound (every group streams its whole B for a few rows), and 1-CTA 128x128
-// tiles spread the B stream over twice the tiles: 77-82% of HBM bandwidth instead of 68-70%
-// on the skinny sweep (bench.py extra skinny_sweep, tools/skinny_tiles.py).  Below 3 rows per
-// group the pair tile measured faster (54 vs 62 us at 1-2 rows).
+// 256x256 tile, unless the groups average at most 128 rows (m_alloc <= 128 G).  Such launches
+// are HBM-bound (every group streams its whole B for a few rows), and 1-CTA 128x128 tiles
+// spread the B stream over twice the tiles: 73-82% of HBM bandwidth instead of 59-70% on the
+// skinny sweep (bench.py extra skinny_sweep, tools/skinny_tiles.py), at every r = 1..127.
+// (1-2 rows per group once favoured the pair tile; that was the 128-row A box over a tiny A,
+// now sized to the tensor.)
 static bool auto_single_cta(int64_t m_alloc, int G, uint32_t flags) {
   if (flags & (TAGG_FLAG_SINGLE_CTA | TAGG_FLAG_TILE_N128 | TAGG_FLAG_TILE_N256))
     return (flags & TAGG_FLAG_SINGLE_CTA) != 0;
-  return m_alloc >= 3ll * G && m_alloc <= static_cast<int64_t>(BM) * G;
+  return m_alloc <= static_cast<int64_t>(BM) * G;
 }
 
 extern "C" int tagg_launch_clusters(int64_t m_alloc, int G, int N, uint32_t flags) {
@@ -1054,23 +1090,23 @@ extern "C" int tagg_grouped_gemm_fp8(const void* a, int64_t lda, const float* sa
                                      const int32_t* group_sizes, int G, int N, int K, void* c, int64_t ldc,
                                      int64_t c_rows, const int64_t* c_row_offsets, int32_t* tile_map,
                                      uint32_t flags, void* stream) {
-  return tagg_grouped_gemm_fp8_checked(a, lda, sa, m_alloc, b, b_layout, b_experts, sb, sb_stride_g, sb_stride_kb,
-                                       sb_stride_nb, group_sizes, G, N, K, c, ldc, c_rows, c_row_offsets, tile_map,
-                                       nullptr, flags, stream);
+  return tagg_grouped_gemm_fp8_ex(a, lda, sa, m_alloc, b, b_layout, b_experts, sb, sb_stride_g, sb_stride_kb,
+                                  sb_stride_nb, group_sizes, G, N, K, c, ldc, c_rows, c_row_offsets, tile_map,
+                                  nullptr, nullptr, flags, stream);
 }
 
-extern "C" int tagg_grouped_gemm_fp8_checked(const void* a, int64_t lda, const float* sa, int64_t m_alloc,
-                                             const void* b, int b_layout, int b_experts, const float* sb,
-                                             int64_t sb_stride_g, int64_t sb_stride_kb, int64_t sb_stride_nb,
-                                             const int32_t* group_sizes, int G, int N, int K, void* c,
-                                             int64_t ldc, int64_t c_rows, const int64_t* c_row_offsets,
-                                             int32_t* tile_map, int32_t* err_flag, uint32_t flags, void* stream) {
+extern "C" int tagg_grouped_gemm_fp8_ex(const void* a, int64_t lda, const float* sa, int64_t m_alloc, const void* b,
+                                        int b_layout, int b_experts, const float* sb, int64_t sb_stride_g,
+                                        int64_t sb_stride_kb, int64_t sb_stride_nb, const int32_t* group_sizes, int G,
+                                        int N, int K, void* c, int64_t ldc, int64_t c_rows,
+                                        const int64_t* c_row_offsets, int32_t* tile_map, const int32_t* b_index,
+                                        int32_t* err_flag, uint32_t flags, void* stream) {
   // ---- ProblemConfig rules (engine.py:77-92) and operand checks (engine.py:132-142)
   if (K < 16 || K % 16 != 0) return TAGG_ERR_CONFIG;
   if (N < 64 || N % 64 != 0) return TAGG_ERR_CONFIG;
   if (G < 1) return TAGG_ERR_CONFIG;
   if (b_layout != TAGG_B_KN && b_layout != TAGG_B_NK) return TAGG_ERR_CONFIG;
-  if (b_experts != 1 && b_experts != G) return TAGG_ERR_SHAPE;
+  if (b_experts < 1 || (b_experts != 1 && b_experts != G && !b_index)) return TAGG_ERR_SHAPE;
   if (m_alloc < 0 || c_rows < 0 || lda < K || ldc < N) return TAGG_ERR_SHAPE;
   if (!a || !sa || !b || !sb || !group_sizes || !c) return TAGG_ERR_SHAPE;
   // ---- global alignment rules (memory.py:27, GLOBAL_ALIGNMENT = 16)
@@ -1107,6 +1143,7 @@ extern "C" int tagg_grouped_gemm_fp8_checked(const void* a, int64_t lda, const f
   p.c_row_offsets = c_row_offsets;
   p.tile_map = tile_map;
   p.err_flag = err_flag;
+  p.one = 1.0f;
   p.trace = g_trace;
   p.m_alloc = m_alloc;
   p.c_rows = c_rows;
@@ -1121,17 +1158,23 @@ extern "C" int tagg_grouped_gemm_fp8_checked(const void* a, int64_t lda, const f
   p.sa_rb = rb;
   p.b_kmajor = (b_layout == TAGG_B_NK) ? 1 : 0;
   p.b_shared = (b_experts == 1) ? 1 : 0;
+  p.b_experts = b_experts;
+  p.b_index = b_index;
   p.dbg = flags & (kDbgNoLoad | kDbgNoPromote | kDbgNoMath);
 
   uint32_t smem_bytes = 0;
   // bits 12-15 of flags cap the stage count (diagnostics); 0 = as many as fit
-  const uint32_t stage_cap = (flags >> 12) & 0xFu;
+  // diagnostics: TAGG_STAGES caps the ring, TAGG_EPI_PASSES=2 forces the 32 KB two-pass staging
+  static const int env_stages = [] { const char* e = std::getenv("TAGG_STAGES"); return e ? std::atoi(e) : 0; }();
+  static const int env_passes = [] { const char* e = std::getenv("TAGG_EPI_PASSES"); return e ? std::atoi(e) : 0; }();
+  uint32_t stage_cap = (flags >> 12) & 0xFu;
+  if (!stage_cap && env_stages > 0) stage_cap = static_cast<uint32_t>(env_stages);
   uint32_t stages = stage_cap ? std::min<uint32_t>(stage_cap, kMaxStages) : kMaxStages;
   // 256-column tiles: a 64 KB C staging (single-pass epilogue, whose TMA stores then
   // overlap the next tile's k-loop) when that still leaves >= 3 pipeline stages
   // (measured: 3 stages feed the MMA as well as 4); else 32 KB and two passes.
   p.epi_passes = 2;
-  if (bn == 256) {
+  if (bn == 256 && env_passes != 2) {
     uint32_t s1 = stages;
     for (; s1 >= 3; --s1)
       if (smem_layout(p, s1, G, rb, num_acc, stage_bytes_b, 2 * kCStagingBytes) <= 232448) break;
@@ -1149,9 +1192,17 @@ extern "C" int tagg_grouped_gemm_fp8_checked(const void* a, int64_t lda, const f
 
   // ---- tensor maps: A, B, and the C store pool (8 heights)
   {
+    // The A box is 128 rows, or pow2ceil(m_alloc) rows for a tensor of fewer rows: the smem rows
+    // past the box keep stale bytes, which only reach accumulator rows that are never stored
+    // (an MMA row depends on its own A row alone).  A 128-row box over an 8-row A -- 120 rows
+    // of out-of-bounds fill per k-block in every CTA -- ran the 1-row skinny sweep at ~60% of
+    // its HBM bound (tools/skinny_malloc.py).
+    uint32_t a_box = BM;
+    while (a_box > 1 && static_cast<int64_t>(a_box / 2) >= m_alloc) a_box /= 2;
+    p.stage_tx = static_cast<uint32_t>(cg) * (a_box * BK + stage_bytes_b);
     const uint64_t dims[2] = {static_cast<uint64_t>(K), static_cast<uint64_t>(m_alloc)};
     const uint64_t str[1] = {static_cast<uint64_t>(lda)};
-    const uint32_t box[2] = {BK, BM};
+    const uint32_t box[2] = {BK, a_box};
     if (!encode(&p.tmap_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, a, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return TAGG_ERR_CUDA;
   }
@@ -1190,6 +1241,16 @@ extern "C" int tagg_grouped_gemm_fp8_checked(const void* a, int64_t lda, const f
   // after that grid completed); TAGG_FLAG_SERIAL restores plain stream order
   const bool pdl = (flags & TAGG_FLAG_SERIAL) == 0;
   p.pdl_overlap = (pdl && (flags & TAGG_FLAG_PDL_OVERLAP)) ? 1u : 0u;
+  {
+    // diagnostics: TAGG_L2_HINT=<a + 4 b>, each 0 none / 1 evict_first / 2 evict_last / 3 evict_normal
+    static const int hint = [] {
+      const char* e = std::getenv("TAGG_L2_HINT");
+      return e ? std::atoi(e) : 0;
+    }();
+    const uint64_t pol[4] = {0, kL2EvictFirst, kL2EvictLast, kL2EvictNormal};
+    p.l2_a = pol[hint & 3];
+    p.l2_b = pol[(hint >> 2) & 3];
+  }
   if (cg == 1) e = launch_cfg<1, 128>(p, smem_bytes, grid, st, exact, swz, pdl);
   else if (bn == 128) e = launch_cfg<2, 128>(p, smem_bytes, grid, st, exact, swz, pdl);
   else e = launch_cfg<2, 256>(p, smem_bytes, grid, st, exact, swz, pdl);

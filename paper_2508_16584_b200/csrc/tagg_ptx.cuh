@@ -176,6 +176,43 @@ __device__ __forceinline__ void tma_load_3d_u32(const CUtensorMap* m, uint32_t b
         "l"(reinterpret_cast<uint64_t>(m)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+// The same loads with an L2 eviction-priority hint (a createpolicy-style 64-bit policy:
+// kL2EvictFirst / kL2EvictLast / kL2EvictNormal).
+constexpr uint64_t kL2EvictNormal = 0x1000000000000000ull;
+constexpr uint64_t kL2EvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kL2EvictLast = 0x14F0000000000000ull;
+template <int kCG>
+__device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* m, uint32_t bar, uint32_t dst, int32_t c0,
+                                                 int32_t c1, uint64_t policy) {
+  if constexpr (kCG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+template <int kCG>
+__device__ __forceinline__ void tma_load_3d_hint(const CUtensorMap* m, uint32_t bar, uint32_t dst, int32_t c0,
+                                                 int32_t c1, int32_t c2, uint64_t policy) {
+  if constexpr (kCG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_load_1d_addr(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -436,6 +473,17 @@ __device__ __forceinline__ void fmul2s(float& d0, float& d1, float a0, float a1,
       "}\n"
       : "=f"(d0), "=f"(d1)
       : "f"(a0), "f"(a1), "f"(s));
+}
+
+// The reference's two roundings on a pair, acc = fl(acc + fl(p * s)) (engine.py:161-164), in two
+// packed instructions: t = FMUL2(p, s), then acc = FFMA2(t, one, acc) = fl(acc + t) exactly
+// (t * 1 is exact).  `one` must be opaque to ptxas (a value it cannot prove is 1.0): it then
+// can neither drop the multiply-by-one nor contract FMUL2 + FADD2 into one FFMA2, which it
+// does for packed mul.rn + add.rn even with -fmad=false.
+__device__ __forceinline__ void fma2_two_roundings(float& c0, float& c1, float p0, float p1, float s, float one) {
+  float t0, t1;
+  fmul2s(t0, t1, p0, p1, s);
+  ffma2v(c0, c1, t0, t1, one, one);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

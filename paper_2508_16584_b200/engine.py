@@ -36,6 +36,7 @@ FLAG_SERIAL = 32  # no programmatic dependent launch (include/tagg.h TAGG_FLAG_S
 FLAG_PDL_OVERLAP = 64  # inputs not written by the previous kernel: overlap its tail (TAGG_FLAG_PDL_OVERLAP)
 ERR_NEGATIVE_SIZE = 1  # device error flag bits (tagg_grouped_gemm_fp8_checked)
 ERR_ROWS_OUT_OF_RANGE = 2
+ERR_B_INDEX = 4
 SM_LIMIT_SHIFT = 16  # TAGG_SM_LIMIT(n): cap the persistent grid at n SMs (include/tagg.h)
 TILES = {None: 0, "auto": 0, "1cta": FLAG_SINGLE_CTA, "pair_n128": FLAG_TILE_N128, "pair_n256": FLAG_TILE_N256}
 TILE_MAP_FIELDS = 9
@@ -193,7 +194,8 @@ def _ptr(t):
 
 def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", out=None, c_row_offsets=None,
                      tile_map=None, exact_promotion=False, plain_staging=False, single_cta=False, tile=None,
-                     stream=None, max_sms=None, pdl=True, pdl_overlap=False, err_flag=None, check=False):
+                     stream=None, max_sms=None, pdl=True, pdl_overlap=False, err_flag=None, check=False,
+                     b_index=None):
     """Padding-free FP8 grouped GEMM on device tensors (no host sync).
 
     a [m_alloc,K] uint8 / float8_e4m3fn; a_scales [m_alloc,ceil(K/128)] f32;
@@ -203,7 +205,10 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
     written; with ``c_row_offsets`` (int64 CUDA [G]) group g's rows start at
     c_row_offsets[g].  ``tile`` picks the tile shape: "pair_n256" (CTA pair,
     256x256), "pair_n128" (CTA pair, 256x128), "1cta" (128x128) or None/"auto" (pair 256x256,
-    or 1-CTA tiles when 3 G <= m_alloc <= 128 G: skinny, HBM-bound groups).
+    or 1-CTA tiles when m_alloc <= 128 G: skinny, HBM-bound groups).
+
+    ``b_index`` (int32 CUDA [G], optional): group g multiplies expert b_index[g] of B, so
+    several groups may share one expert (an all-to-all's (source, expert) segments).
 
     Group sizes never reach the host, so the kernel validates them: a negative M_g or
     more rows than A / ``out`` hold makes the launch write nothing and OR-s a bit into
@@ -259,6 +264,12 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
         raise ConfigError(f"b_layout must be 'kn' or 'nk', got {b_layout!r}")
     if not b.is_contiguous():
         raise ShapeMismatch("B must be contiguous")
+    if b_index is not None:
+        if b_index.dtype != torch.int32 or not b_index.is_cuda or b_index.numel() != G:
+            raise ShapeMismatch(f"b_index must be an int32 CUDA tensor of {G} entries")
+        b_index = b_index.contiguous()
+    elif b_experts not in (1, G):
+        raise ShapeMismatch(f"B holds {b_experts} experts for {G} groups (give b_index)")
     if out is None:
         out = torch.empty((m_alloc, N), dtype=torch.bfloat16, device=a.device)
     if out.dtype not in (torch.bfloat16, torch.uint16, torch.int16) or out.stride(1) != 1 or out.dim() != 2:
@@ -281,10 +292,10 @@ def grouped_gemm_fp8(a, a_scales, b, b_scales, group_sizes, *, b_layout="kn", ou
         err_flag = torch.zeros(1, dtype=torch.int32, device=a.device)
     if err_flag is not None and (err_flag.dtype != torch.int32 or not err_flag.is_cuda):
         raise ShapeMismatch("err_flag must be an int32 CUDA tensor")
-    rc = lib().tagg_grouped_gemm_fp8_checked(
+    rc = lib().tagg_grouped_gemm_fp8_ex(
         _ptr(a), a.stride(0), _ptr(a_scales), m_alloc, _ptr(b), layout, b_experts, _ptr(b_scales),
         sb_g, sb_kb, sb_nb, _ptr(group_sizes), G, N, K, _ptr(out), out.stride(0), out.shape[0],
-        _ptr(c_row_offsets), _ptr(tile_map), _ptr(err_flag), flags, st.cuda_stream)
+        _ptr(c_row_offsets), _ptr(tile_map), _ptr(b_index), _ptr(err_flag), flags, st.cuda_stream)
     raise_for_status(rc, "tagg_grouped_gemm_fp8")
     if check:
         raise_for_device_flag(int(err_flag.item()), "tagg_grouped_gemm_fp8")
@@ -297,6 +308,8 @@ def raise_for_device_flag(bits: int, what: str) -> None:
         raise ConfigError(f"{what}: group sizes must be non-negative")
     if bits & ERR_ROWS_OUT_OF_RANGE:
         raise ShapeMismatch(f"{what}: sum of group sizes exceeds the rows of A / out")
+    if bits & ERR_B_INDEX:
+        raise ShapeMismatch(f"{what}: b_index names an expert outside B")
 
 
 def max_tiles(m_alloc: int, groups: int, n: int) -> int:

@@ -12,11 +12,14 @@ dispatch():
   2. all_to_all_single of the int32 counts (every rank learns what it receives)
   3. one host read of the split sizes (the only sync)
   4. all_to_all_single of the FP8 rows [rows, K] and their 1x128 scales [rows, kb]
-  5. a device permutation from (source rank, expert) order to expert-contiguous
-     order, which is the padding-free grouped layout the kernel consumes, with
-     no rows added
+  5. in_place=False: a device permutation from (source rank, expert) order to
+     expert-contiguous order (one group per local expert).  in_place=True (what the
+     pipelined path uses): no permutation -- every (source rank, expert) segment is a
+     group of its own and meta.b_index names its expert, so the grouped GEMM reads the
+     received rows where they landed and writes C in the order combine() sends back
+     (tagg_grouped_gemm_fp8_ex's b_index).
 combine() reverses steps 5 and 4 on the bf16 outputs and restores the original
-(token, k) order.
+(token, k) order.  At world size 1 the all-to-alls are identities and are skipped.
 
 The transport is torch.distributed, NCCL on GPUs (NVLink 5 / NVSwitch) and
 gloo on CPU (tests).  No reference counterpart exists: the reference is
@@ -44,6 +47,7 @@ class DispatchMeta:
     experts_per_rank: int
     from_grouped: torch.Tensor | None = None  # inverse of to_grouped
     inv_order: torch.Tensor | None = None     # inverse of order: sorted position of each local row
+    b_index: torch.Tensor | None = None       # in_place: int32 [P * E_local] expert of each segment group
 
 
 def _inverse(perm: torch.Tensor) -> torch.Tensor:
@@ -59,13 +63,15 @@ def _counts(expert_ids: torch.Tensor, num_experts: int) -> torch.Tensor:
 
 
 def dispatch(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_ids: torch.Tensor, num_experts: int,
-             group=None):
+             group=None, in_place: bool = False):
     """Send each routed row to the rank that owns its expert.
 
     a_codes [R, K] uint8 / float8_e4m3fn, a_scales [R, kb] f32, expert_ids [R]
     (one expert per row; a top-k router flattens (token, k) into rows).
     Returns (a_local, sa_local, meta).  a_local is in expert-contiguous order
-    for this rank's experts and meta.group_sizes holds the device group sizes.
+    for this rank's experts and meta.group_sizes holds the device group sizes.  With
+    ``in_place`` the rows stay in arrival order, (source rank, expert) segments: then
+    meta.group_sizes has one entry per segment and meta.b_index its expert.
     """
     world = dist.get_world_size(group)
     if num_experts % world:
@@ -77,10 +83,11 @@ def dispatch(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_ids: torch.Te
     a_sorted = a_codes.index_select(0, order)
     sa_sorted = a_scales.index_select(0, order)
     counts = _counts(expert_ids, num_experts)                       # [E] rows per expert, local
-    return _exchange(a_sorted, sa_sorted, counts, order, epr, group)
+    return _exchange(a_sorted, sa_sorted, counts, order, epr, group, in_place=in_place)
 
 
-def dispatch_tokens(x: torch.Tensor, expert_ids: torch.Tensor, num_experts: int, group=None):
+def dispatch_tokens(x: torch.Tensor, expert_ids: torch.Tensor, num_experts: int, group=None,
+                    in_place: bool = False):
     """Quantize-and-dispatch from bf16/f32 activations (SURVEY.md §8f ranks 1+3).
 
     x [T, K] activations, expert_ids [T, topk].  The fused kernel (quant.quantize_dispatch)
@@ -98,11 +105,25 @@ def dispatch_tokens(x: torch.Tensor, expert_ids: torch.Tensor, num_experts: int,
     order = torch.empty_like(d.dest_rows, dtype=torch.int64)       # sorted row -> local (t, k) row
     order[d.dest_rows.to(torch.int64)] = torch.arange(d.dest_rows.numel(), device=x.device)
     return _exchange(d.a_codes.contiguous(), d.a_scales, d.group_sizes, order, num_experts // world, group,
-                     inv_order=d.dest_rows.to(torch.int64))
+                     inv_order=d.dest_rows.to(torch.int64), in_place=in_place)
 
 
-def _exchange(a_sorted, sa_sorted, counts, order, epr, group, inv_order=None):
-    """All-to-all of expert-sorted local rows; regroup received rows to expert-contiguous."""
+def _a2a(out, inp, out_splits, in_splits, group):
+    """all_to_all_single, skipped at world size 1 where it is the identity (a full-size copy)."""
+    if dist.get_world_size(group) == 1:
+        return inp
+    dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+    return out
+
+
+def segment_b_index(world: int, epr: int, device) -> torch.Tensor:
+    """Expert (local index) of each (source rank, expert) segment group, source-major."""
+    return (torch.arange(world * epr, device=device, dtype=torch.int32) % epr).contiguous()
+
+
+def _exchange(a_sorted, sa_sorted, counts, order, epr, group, inv_order=None, in_place=False):
+    """All-to-all of expert-sorted local rows; regroup received rows to expert-contiguous
+    (or, in_place, leave them as (source, expert) segment groups)."""
     world = dist.get_world_size(group)
     dev = a_sorted.device
     a_codes, a_scales = a_sorted, sa_sorted
@@ -114,10 +135,15 @@ def _exchange(a_sorted, sa_sorted, counts, order, epr, group, inv_order=None):
     both = torch.cat([send_splits, recv_splits_t]).cpu().tolist()   # the one host sync
     send_splits, recv_splits = both[:world], both[world:]
     n_recv = sum(recv_splits)
-    a_recv = torch.empty((n_recv, a_codes.shape[1]), dtype=torch.uint8, device=dev)
-    sa_recv = torch.empty((n_recv, a_scales.shape[1]), dtype=a_scales.dtype, device=dev)
-    dist.all_to_all_single(a_recv, a_sorted.contiguous(), recv_splits, send_splits, group=group)
-    dist.all_to_all_single(sa_recv, sa_sorted.contiguous(), recv_splits, send_splits, group=group)
+    a_recv = torch.empty((n_recv, a_codes.shape[1]), dtype=torch.uint8, device=dev) if world > 1 else None
+    sa_recv = torch.empty((n_recv, a_scales.shape[1]), dtype=a_scales.dtype, device=dev) if world > 1 else None
+    a_recv = _a2a(a_recv, a_sorted.contiguous(), recv_splits, send_splits, group)
+    sa_recv = _a2a(sa_recv, sa_sorted.contiguous(), recv_splits, send_splits, group)
+    if in_place:
+        meta = DispatchMeta(order, send_splits, recv_splits, None, recv_mat.reshape(-1).to(torch.int32).contiguous(),
+                            epr, inv_order=_inverse(order) if inv_order is None else inv_order,
+                            b_index=segment_b_index(world, epr, dev))
+        return a_recv, sa_recv, meta
     # received rows are ordered (src, expert); regroup them to (expert, src)
     src_off = torch.cumsum(recv_mat.reshape(-1).to(torch.int64), 0) - recv_mat.reshape(-1).to(torch.int64)
     src_off = src_off.view(world, epr)
@@ -137,9 +163,13 @@ def _exchange(a_sorted, sa_sorted, counts, order, epr, group, inv_order=None):
 
 def combine(c_local: torch.Tensor, meta: DispatchMeta, group=None) -> torch.Tensor:
     """Return grouped outputs [rows_local, N] to the ranks and rows they came from."""
-    c_recv_order = c_local.index_select(0, meta.from_grouped)
-    out_sorted = torch.empty((sum(meta.send_splits), c_local.shape[1]), dtype=c_local.dtype, device=c_local.device)
-    dist.all_to_all_single(out_sorted, c_recv_order, meta.send_splits, meta.recv_splits, group=group)
+    c_recv_order = c_local if meta.from_grouped is None else c_local.index_select(0, meta.from_grouped)
+    world = dist.get_world_size(group)
+    out_sorted = None
+    if world > 1:
+        out_sorted = torch.empty((sum(meta.send_splits), c_local.shape[1]), dtype=c_local.dtype,
+                                 device=c_local.device)
+    out_sorted = _a2a(out_sorted, c_recv_order, meta.send_splits, meta.recv_splits, group)
     return out_sorted.index_select(0, meta.inv_order)
 
 
@@ -166,6 +196,8 @@ class ChunkPlan:
     inv_order: torch.Tensor        # inverse of order
     group_sizes: list              # [C] int32 [E_local] device group sizes of chunk c
     experts_per_rank: int
+    seg_sizes: list | None = None  # [C] int32 [P * E_local]: chunk c's (source rank, expert) segments
+    b_index: torch.Tensor | None = None  # int32 [P * E_local]: the expert of each segment
 
     @property
     def recv_rows(self) -> list:
@@ -213,8 +245,10 @@ def plan_chunks(expert_ids: torch.Tensor, num_experts: int, chunks: int, group=N
         send_off.append(send_off[-1] + sum(send_splits[c]))
     to_grouped = [_regroup_index(recv[:, c, :], sum(recv_splits[c])) for c in range(chunks)]
     group_sizes = [recv[:, c, :].sum(0).to(torch.int32) for c in range(chunks)]
+    seg_sizes = [recv[:, c, :].reshape(-1).to(torch.int32).contiguous() for c in range(chunks)]
     return ChunkPlan(chunks, order, send_splits, recv_splits, send_off, to_grouped,
-                     [_inverse(t) for t in to_grouped], _inverse(order), group_sizes, epr)
+                     [_inverse(t) for t in to_grouped], _inverse(order), group_sizes, epr, seg_sizes,
+                     segment_b_index(world, epr, dev))
 
 
 _COMM_STREAMS: dict = {}
@@ -230,13 +264,21 @@ def _comm_stream(dev: torch.device):
 
 def pipelined_expert_gemm(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_ids: torch.Tensor,
                           num_experts: int, expert_gemm, n_out: int, *, chunks: int = 4, group=None,
-                          comm_stream=None, out_dtype=torch.bfloat16, plan: ChunkPlan | None = None):
+                          comm_stream=None, out_dtype=torch.bfloat16, plan: ChunkPlan | None = None,
+                          in_place: bool = True):
     """Dispatch -> per-expert GEMM -> combine, pipelined over row chunks.
 
     a_codes [R, K] e4m3 codes, a_scales [R, kb] f32 and expert_ids [R] are this rank's routed
     rows (dispatch() semantics).  ``expert_gemm(codes, scales, group_sizes) -> [rows, n_out]``
     runs this rank's experts on one chunk's rows in the padding-free grouped layout (codes may
     be a row-strided view).  Returns [R, n_out]: every row's output back in local row order.
+
+    With ``in_place`` (default) the GEMM reads each chunk's received rows where they landed:
+    ``expert_gemm(codes, scales, group_sizes, b_index=..., out=...)`` gets one group per
+    (source rank, expert) segment, b_index naming the expert, and writes its result straight
+    into the buffer the return all-to-all sends (tagg_grouped_gemm_fp8_ex's b_index), so no
+    row is permuted between the exchanges.  in_place=False regroups each chunk to one group
+    per expert first and back after (3-argument expert_gemm).
 
     Codes and scales travel packed in one all-to-all per chunk (K + 4*kb bytes a row, padded
     to 16).  On CUDA the all-to-alls run on ``comm_stream``: chunk c's GEMM overlaps chunk
@@ -262,10 +304,11 @@ def pipelined_expert_gemm(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_
     packed = torch.empty((rows, width), dtype=torch.uint8, device=dev)
     packed[:, :k] = a_codes.index_select(0, plan.order)
     packed[:, k:k + 4 * kb] = a_scales.contiguous().index_select(0, plan.order).view(torch.uint8)
-    recv_all = torch.empty((recv_off[-1], width), dtype=torch.uint8, device=dev)
-    grouped_all = torch.empty_like(recv_all)
+    world = dist.get_world_size(group)
+    recv_all = torch.empty((recv_off[-1], width), dtype=torch.uint8, device=dev) if world > 1 else packed
+    grouped_all = None if in_place else torch.empty_like(recv_all)
     back_all = torch.empty((recv_off[-1], n_out), dtype=out_dtype, device=dev)
-    out_sorted = torch.empty((rows, n_out), dtype=out_dtype, device=dev)
+    out_sorted = back_all if world == 1 else torch.empty((rows, n_out), dtype=out_dtype, device=dev)
 
     def on(stream):
         return torch.cuda.stream(stream) if cuda else contextlib.nullcontext()
@@ -277,12 +320,16 @@ def pipelined_expert_gemm(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_
 
     def send_chunk(c):
         with on(comm):
-            dist.all_to_all_single(recv_all[recv_off[c]:recv_off[c + 1]], packed[plan.send_off[c]:plan.send_off[c + 1]],
-                                   plan.recv_splits[c], plan.send_splits[c], group=group)
+            if world > 1:  # at world size 1 the received rows are the packed rows themselves
+                dist.all_to_all_single(recv_all[recv_off[c]:recv_off[c + 1]],
+                                       packed[plan.send_off[c]:plan.send_off[c + 1]], plan.recv_splits[c],
+                                       plan.send_splits[c], group=group)
             if cuda:
                 arrived[c].record(comm)
 
     def return_chunk(c):
+        if world == 1:
+            return  # back_all is out_sorted (below)
         with on(comm):
             if cuda:
                 comm.wait_event(done[c])
@@ -295,7 +342,13 @@ def pipelined_expert_gemm(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_
         if cuda:
             compute.wait_event(arrived[c])
         lo, hi = recv_off[c], recv_off[c + 1]
-        if hi > lo:
+        if hi > lo and in_place:
+            rows_c = recv_all[lo:hi]
+            y = expert_gemm(rows_c[:, :k], rows_c[:, k:k + 4 * kb].contiguous().view(torch.float32),
+                            plan.seg_sizes[c], b_index=plan.b_index, out=back_all[lo:hi])
+            if y.data_ptr() != back_all[lo:hi].data_ptr():
+                back_all[lo:hi].copy_(y[:hi - lo])
+        elif hi > lo:
             grouped = grouped_all[lo:hi]
             torch.index_select(recv_all[lo:hi], 0, plan.to_grouped[c], out=grouped)  # padding-free grouped layout
             y = expert_gemm(grouped[:, :k], grouped[:, k:k + 4 * kb].contiguous().view(torch.float32),
@@ -308,7 +361,7 @@ def pipelined_expert_gemm(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_
         return_chunk(c)
     if cuda:
         compute.wait_stream(comm)
-        for t in (packed, recv_all, back_all, out_sorted):
+        for t in {id(x): x for x in (packed, recv_all, back_all, out_sorted)}.values():
             t.record_stream(comm)
     return out_sorted.index_select(0, plan.inv_order)
 

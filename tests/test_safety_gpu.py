@@ -193,3 +193,32 @@ def test_dropped_routes_are_skipped_end_to_end():
     cb = c.view(torch.int16).cpu().numpy().view(np.uint16)
     want = omoe.combine(cb, np.where(dest < 0, 0, dest), np.where(ok.reshape(tokens, topk), w.cpu().numpy(), 0))
     np.testing.assert_array_equal(y.view(torch.int16).cpu().numpy().view(np.uint16), want)
+
+
+@pytest.mark.parametrize("layout", ["kn", "nk"])
+@pytest.mark.parametrize("tile", [None, "1cta", "pair_n256"])
+def test_b_index_groups_share_experts(layout, tile):
+    """tagg_grouped_gemm_fp8_ex's b_index: 7 groups over 3 experts (the (source, expert)
+    segments of an all-to-all).  Equals the oracle with each group's expert B spelled out."""
+    sizes = (100, 0, 257, 3, 128, 64, 300)
+    bidx = (2, 0, 1, 2, 0, 1, 1)
+    n, k = 256, 384
+    m = sum(sizes)
+    g = torch.Generator(device=DEV).manual_seed(17)
+    a = torch.randint(0, 0x7E, (m, k), dtype=torch.uint8, device=DEV, generator=g)
+    sa = torch.rand((m, k // 128), device=DEV, generator=g) + 0.5
+    shape = (3, k, n) if layout == "kn" else (3, n, k)
+    sshape = (3, k // 128, n // 128) if layout == "kn" else (3, n // 128, k // 128)
+    b = torch.randint(0, 0x7E, shape, dtype=torch.uint8, device=DEV, generator=g)
+    sb = torch.rand(sshape, device=DEV, generator=g) + 0.5
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    bi = torch.tensor(bidx, dtype=torch.int32, device=DEV)
+    out = tg.grouped_gemm_fp8(a, sa, b, sb, gs, b_layout=layout, b_index=bi, tile=tile, check=True)
+    bn, sbn = b.cpu().numpy()[list(bidx)], sb.cpu().numpy()[list(bidx)]
+    want = oracle_c(a.cpu().numpy(), sa.cpu().numpy(), bn, sbn, sizes, b_layout=layout)
+    assert_parity(out.view(torch.int16).cpu().numpy().view(np.uint16), want)
+    bad = torch.tensor((2, 0, 1, 3, 0, 1, 1), dtype=torch.int32, device=DEV)  # expert 3 of 3
+    with pytest.raises(tg.ShapeMismatch):
+        tg.grouped_gemm_fp8(a, sa, b, sb, gs, b_layout=layout, b_index=bad, tile=tile, check=True)
+    ok_empty = torch.tensor((2, 99, 1, 2, 0, 1, 1), dtype=torch.int32, device=DEV)  # empty group: ignored
+    tg.grouped_gemm_fp8(a, sa, b, sb, gs, b_layout=layout, b_index=ok_empty, tile=tile, check=True)

@@ -3,7 +3,7 @@ sys.path.insert(0, ".")
 import bench, paper_2508_16584_b200 as tg
 dev = torch.device("cuda", 0)
 hbm = bench._peaks()[0]["hbm_gbs"]
-for r in (3, 4, 6, 16):
+for r in (1, 2, 3, 8):
     P = bench.Problem(torch, "s", [tuple([r] * 8)], 4096, 7168, 8, dev, seed=r)
     gs = P.gs[0]
     nb = P.algorithmic_bytes(P.sizes_list[0])
