@@ -995,8 +995,10 @@ def run_ep_down(torch, dist, tg, dev, rank, world, fp8_peak, exact, iters=5, war
         state["back"] = ep.combine(state["out"][:m], state["meta"])
 
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    gemm_sms = sms - 16  # the overlapped path leaves 16 SMs to the NCCL kernels
-    chunks = 4
+    # At world 1 there is no exchange to hide: one chunk on every SM (each further chunk would
+    # re-read all of B).  Across GPUs, 4 chunks with 16 SMs left to the NCCL kernels.
+    gemm_sms = sms if world == 1 else sms - 16
+    chunks = 1 if world == 1 else 4
 
     def capped(codes, scales, gs, b_index=None, out=None):
         return tg.grouped_gemm_fp8(codes, scales, b, sb, gs, exact_promotion=exact, max_sms=gemm_sms,

@@ -47,6 +47,20 @@ __device__ void build_pad_tables(const int32_t* gs, int G, int32_t* row_off, int
   __syncthreads();
 }
 
+// A row copy by one warp: 4 16-byte vectors per lane in flight (loads first, then stores), so a
+// warp keeps 2 KB of reads outstanding instead of one 512-byte wave at a time.
+__device__ __forceinline__ void copy_row(uint4* __restrict__ dst, const uint4* __restrict__ src, int vec, int lane) {
+  int i = lane;
+  for (; i + 96 < vec; i += 128) {
+    const uint4 v0 = __ldg(src + i), v1 = __ldg(src + i + 32), v2 = __ldg(src + i + 64), v3 = __ldg(src + i + 96);
+    dst[i] = v0;
+    dst[i + 32] = v1;
+    dst[i + 64] = v2;
+    dst[i + 96] = v3;
+  }
+  for (; i < vec; i += 32) dst[i] = __ldg(src + i);
+}
+
 __device__ __forceinline__ int find_group(const int32_t* off, int G, int x) {
   int lo = 0, hi = G - 1;  // largest g with off[g] <= x
   while (lo < hi) {
@@ -81,8 +95,7 @@ __global__ void __launch_bounds__(256) pad_groups_kernel(const uint8_t* __restri
     float* dsa = sa_pad + p * kbc;
     if (local < size[g]) {
       const int64_t src_row = row_off[g] + local;
-      const uint4* src = reinterpret_cast<const uint4*>(a + src_row * lda);
-      for (int i = lane; i < vec; i += 32) dst[i] = __ldg(src + i);
+      copy_row(dst, reinterpret_cast<const uint4*>(a + src_row * lda), vec, lane);
       const float* ssa = sa + src_row * kbc;
       for (int i = lane; i < kbc; i += 32) dsa[i] = __ldg(ssa + i);
     } else {
@@ -109,16 +122,18 @@ __global__ void __launch_bounds__(256) unpad_rows_kernel(const uint16_t* __restr
     const int g = find_group(row_off, G, static_cast<int>(r));
     const int64_t src_row = pad_off[g] + (r - row_off[g]);
     const uint4* src = reinterpret_cast<const uint4*>(c_pad + src_row * N);
-    uint4* dst = reinterpret_cast<uint4*>(c + r * N);
-    for (int i = lane; i < vec; i += 32) dst[i] = __ldg(src + i);
+    copy_row(reinterpret_cast<uint4*>(c + r * N), src, vec, lane);
   }
   (void)size;
 }
 
-static int grid_for_device() {
+// 4 CTAs (32 warps) per SM, but no more CTAs than the rows give warps to (one warp per row):
+// a launch over a few rows then does not spend its time building 592 CTAs' group tables.
+static int grid_for_rows(int64_t rows) {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return 4 * n;
+  const int64_t want = (rows + 7) / 8;
+  return static_cast<int>(want < 1 ? 1 : (want < 4 * n ? want : 4 * n));
 }
 
 }  // namespace tagg
@@ -137,7 +152,7 @@ extern "C" int tagg_pad_groups(const void* a, int64_t lda, const float* sa, cons
   const int kbc = (K + 127) / 128;
   const size_t shm = sizeof(int32_t) * (3 * G + 2);
   if (shm > 48 * 1024) return TAGG_ERR_UNSUPPORTED;
-  tagg::pad_groups_kernel<<<tagg::grid_for_device(), 256, shm, static_cast<cudaStream_t>(stream)>>>(
+  tagg::pad_groups_kernel<<<tagg::grid_for_rows(m_pad_alloc), 256, shm, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(a), lda, sa, group_sizes, G, K, kbc, static_cast<uint8_t*>(a_pad), sa_pad,
       padded_sizes, m_pad_alloc);
   return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
@@ -150,7 +165,7 @@ extern "C" int tagg_unpad_rows(const void* c_pad, const int32_t* group_sizes, in
   if ((reinterpret_cast<uintptr_t>(c_pad) | reinterpret_cast<uintptr_t>(c)) & 15u) return TAGG_ERR_ALIGNMENT;
   const size_t shm = sizeof(int32_t) * (3 * G + 2);
   if (shm > 48 * 1024) return TAGG_ERR_UNSUPPORTED;
-  tagg::unpad_rows_kernel<<<tagg::grid_for_device(), 256, shm, static_cast<cudaStream_t>(stream)>>>(
+  tagg::unpad_rows_kernel<<<tagg::grid_for_rows(m_alloc), 256, shm, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(c_pad), group_sizes, G, N, static_cast<uint16_t*>(c), m_alloc);
   return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
 }

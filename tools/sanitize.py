@@ -36,6 +36,19 @@ tg.quantize_blocks(torch.randn((2, 256, 384), device=dev))
 xc, xs = tg.quantize_col_blocks(torch.randn((m, 256), device=dev), gs)
 dyc, dys = tg.quantize_col_blocks(torch.randn((m, 128), device=dev), gs)
 tg.wgrad_fp8(xc, xs, dyc, dys, gs)
+# bf16 column quantizer (persistent kernel), plain and gathered
+xb = torch.randn((m, 512), device=dev).to(torch.bfloat16)
+tg.quantize_col_blocks(xb, gs)
+idx = torch.randperm(m, device=dev).to(torch.int32)
+tg.quantize_col_blocks(xb, gs, index=idx, row_weights=torch.rand(m, device=dev))
+# groups sharing experts (b_index), the device error flag, a PDL-overlap chain into one output
+bi = torch.tensor([1, 0, 2, 1, 5, 3], dtype=torch.int32, device=dev)
+tg.grouped_gemm_fp8(a, sa, b, sb, gs, b_index=bi, check=True)
+flag = torch.zeros(1, dtype=torch.int32, device=dev)
+tg.grouped_gemm_fp8(a, sa, b, sb, torch.tensor([5000, 1, 0, 0, 0, 0], dtype=torch.int32, device=dev),
+                    err_flag=flag)
+for _ in range(3):
+    tg.grouped_gemm_fp8(a, sa, b, sb, gs, out=out[:m] if False else None, pdl_overlap=True)
 from paper_2508_16584_b200 import moe  # noqa: E402
 
 h = torch.randn((m + 40, 512), device=dev).to(torch.bfloat16)
