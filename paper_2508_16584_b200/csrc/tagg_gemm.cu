@@ -382,8 +382,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         const uint32_t dst0 = sSB0 + sab * kSbBufBytes;
 #pragma unroll
         for (int c = 0; c < kSbCols; ++c) {
-          const int nb = (T.n0 >> 7) + c;
-          if (T.n0 + 128 * c >= p.N) break;
+          // a column block past N (the right half of an edge tile) repeats the last valid one:
+          // every slot is rewritten each tile, so the promotion never reads a stale slot
+          const int nb = min((T.n0 >> 7) + c, (p.N - 1) >> 7);
           for (int kb = lane; kb < kbc; kb += 32)
             cp_async_4(dst0 + 4u * (c * kbc + kb), sbg + static_cast<int64_t>(kb) * p.sb_skb +
                                                        static_cast<int64_t>(nb) * p.sb_snb);

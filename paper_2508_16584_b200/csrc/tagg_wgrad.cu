@@ -528,150 +528,6 @@ __global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* 
   if (bad) atomicOr(err, 2);
 }
 
-// Persistent form of the vector quantizer.  The two-pass v8 kernel above launches one CTA per
-// (token block, 512 columns) and keeps ~32 of them resident per SM: ~600 MB of blocks are live
-// between a block's amax pass and its code pass, so the second pass misses the 126 MB L2 and
-// x is read from HBM twice.  Here a grid of 2 CTAs per SM loops over the same units with 16
-// rows of loads in flight per thread: ~76 MB live, so the code pass re-reads from L2.  The
-// (group, token block) table is built once per CTA in shared memory.
-constexpr int kQcThreads = 128;  // 8 columns per thread: 1024 columns per unit
-constexpr int kQcBurst = 16;     // rows of 16-byte loads in flight per thread
-template <bool kBf16>
-__global__ void __launch_bounds__(kQcThreads) quantize_col_blocks_p_kernel(
-    const void* __restrict__ x, int64_t ldx, int cols, const int32_t* __restrict__ group_sizes, int G,
-    uint8_t* __restrict__ codes, int64_t ldc, float* __restrict__ scales, int32_t* err,
-    const int32_t* __restrict__ index, const float* __restrict__ row_weights, int tb_bound) {
-  extern __shared__ int32_t qtab[];
-  int32_t* q_row0 = qtab;              // [tb_bound] first grouped row of token block tb
-  int32_t* q_rows = q_row0 + tb_bound; // [tb_bound] its rows (<= 128)
-  int32_t* g_row = q_rows + tb_bound;  // [G] first row of group g
-  int32_t* g_blk = g_row + G;          // [G + 1] first token block of group g
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int cr = 0, cb = 0;
-    for (int base = 0; base < G; base += 32) {
-      const int g = base + lane;
-      const int m = (g < G) ? max(0, group_sizes[g]) : 0;
-      const int nb = (m + 127) / 128;
-      int im = m, ib = nb;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, im, o);
-        const int b = __shfl_up_sync(0xffffffffu, ib, o);
-        if (lane >= o) { im += a; ib += b; }
-      }
-      if (g < G) {
-        g_row[g] = cr + im - m;
-        g_blk[g] = cb + ib - nb;
-      }
-      cr += __shfl_sync(0xffffffffu, im, 31);
-      cb += __shfl_sync(0xffffffffu, ib, 31);
-    }
-    if (lane == 0) g_blk[G] = min(cb, tb_bound);
-  }
-  __syncthreads();
-  for (int g = threadIdx.x; g < G; g += blockDim.x) {
-    const int m = max(0, group_sizes[g]);
-    for (int b = g_blk[g], j = 0; b < g_blk[g + 1]; ++b, ++j) {
-      q_row0[b] = g_row[g] + 128 * j;
-      q_rows[b] = min(128, m - 128 * j);
-    }
-  }
-  __syncthreads();
-  const int n_tb = g_blk[G];
-  const int cbs = (cols / 8 + kQcThreads - 1) / kQcThreads;
-  const int64_t units = static_cast<int64_t>(n_tb) * cbs;
-  bool bad = false;
-  auto load8 = [&](int64_t r_grouped, int c0, uint4& q, float& wr) {
-    const int64_t rr = index ? static_cast<int64_t>(index[r_grouped]) : r_grouped;
-    wr = row_weights ? row_weights[r_grouped] : 1.0f;
-    if constexpr (kBf16) {
-      q = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + rr * ldx + c0));
-    } else {
-      q = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(x) + rr * ldx + c0));
-    }
-  };
-  auto unpack8 = [&](int64_t r_grouped, int c0, const uint4& q0, float wr, float (&v)[8]) {
-    if constexpr (kBf16) {
-      const uint32_t w[4] = {q0.x, q0.y, q0.z, q0.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        v[2 * j] = __uint_as_float(w[j] << 16);
-        v[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
-      }
-    } else {
-      const int64_t rr = index ? static_cast<int64_t>(index[r_grouped]) : r_grouped;
-      const float4 b = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + rr * ldx + c0) + 1);
-      v[0] = __uint_as_float(q0.x); v[1] = __uint_as_float(q0.y); v[2] = __uint_as_float(q0.z);
-      v[3] = __uint_as_float(q0.w); v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    }
-    if (row_weights) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __fmul_rn(wr, v[j]);
-    }
-  };
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const int tb = static_cast<int>(u / cbs);
-    const int c0 = (static_cast<int>(u % cbs) * kQcThreads + static_cast<int>(threadIdx.x)) * 8;
-    if (c0 >= cols) continue;
-    const int64_t row0 = q_row0[tb];
-    const int rows = q_rows[tb];
-    float amax[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) amax[j] = 0.0f;
-    for (int i0 = 0; i0 < rows; i0 += kQcBurst) {
-      uint4 q[kQcBurst];
-      float wr[kQcBurst];
-#pragma unroll
-      for (int i = 0; i < kQcBurst; ++i)
-        if (i0 + i < rows) load8(row0 + i0 + i, c0, q[i], wr[i]);
-#pragma unroll
-      for (int i = 0; i < kQcBurst; ++i) {
-        if (i0 + i >= rows) break;
-        float v[8];
-        unpack8(row0 + i0 + i, c0, q[i], wr[i], v);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float m = fabsf(v[j]);
-          bad |= !(m <= 3.402823466e38f);
-          amax[j] = fmaxf(amax[j], m);
-        }
-      }
-    }
-    float sc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) sc[j] = amax[j] > 0.0f ? __fdiv_rn(amax[j], 448.0f) : 1.0f;
-    float4* sdst = reinterpret_cast<float4*>(scales + static_cast<int64_t>(tb) * cols + c0);
-    sdst[0] = make_float4(sc[0], sc[1], sc[2], sc[3]);
-    sdst[1] = make_float4(sc[4], sc[5], sc[6], sc[7]);
-    for (int i0 = 0; i0 < rows; i0 += kQcBurst) {
-      uint4 q[kQcBurst];
-      float wr[kQcBurst];
-#pragma unroll
-      for (int i = 0; i < kQcBurst; ++i)
-        if (i0 + i < rows) load8(row0 + i0 + i, c0, q[i], wr[i]);
-#pragma unroll
-      for (int i = 0; i < kQcBurst; ++i) {
-        if (i0 + i >= rows) break;
-        float v[8];
-        unpack8(row0 + i0 + i, c0, q[i], wr[i], v);
-        uint32_t w[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint16_t lo, hi;
-          const float a0 = __fdiv_rn(v[4 * h], sc[4 * h]), a1 = __fdiv_rn(v[4 * h + 1], sc[4 * h + 1]);
-          const float a2 = __fdiv_rn(v[4 * h + 2], sc[4 * h + 2]), a3 = __fdiv_rn(v[4 * h + 3], sc[4 * h + 3]);
-          asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(a1), "f"(a0));
-          asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(a3), "f"(a2));
-          w[h] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
-        }
-        *reinterpret_cast<uint2*>(codes + (row0 + i0 + i) * ldc + c0) = make_uint2(w[0], w[1]);
-      }
-    }
-  }
-  if (bad) atomicOr(err, 2);
-}
-
 }  // namespace wg
 }  // namespace tagg
 
@@ -718,21 +574,6 @@ static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc,
   const int esz = x_dtype == TAGG_DTYPE_BF16 ? 2 : 4;
   const bool v8 = cols % 8 == 0 && !(reinterpret_cast<uintptr_t>(x) % 16) && !((ldx * esz) % 16) &&
                   !(reinterpret_cast<uintptr_t>(codes) % 8) && !(ldc % 8) && !(reinterpret_cast<uintptr_t>(scales) % 16);
-  // the persistent quantizer: bf16 input (the MoE backward's activations and gradients), its
-  // block table in <= 48 KB of shared memory
-  const size_t qc_smem = sizeof(int32_t) * (2 * static_cast<size_t>(tb) + 2 * static_cast<size_t>(G) + 1);
-  static const bool env_old = std::getenv("TAGG_COLQ_V8") != nullptr;  // diagnostics: the two-pass v8 kernel
-  if (v8 && x_dtype == TAGG_DTYPE_BF16 && qc_smem <= 48 * 1024 && !env_old) {
-    const int sms = sm_count();
-    if (sms <= 0) return TAGG_ERR_CUDA;
-    const int64_t cbs = (cols / 8 + wg::kQcThreads - 1) / wg::kQcThreads;
-    const int64_t units = tb * cbs;
-    const int grid = static_cast<int>(std::min<int64_t>(units, 2ll * sms));
-    wg::quantize_col_blocks_p_kernel<true><<<grid, wg::kQcThreads, qc_smem, st>>>(
-        x, ldx, cols, group_sizes, G, static_cast<uint8_t*>(codes), ldc, scales, err_flag, index, row_weights,
-        static_cast<int>(tb));
-    return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
-  }
   if (v8) {
     const dim3 g8(static_cast<unsigned>((cols / 8 + 63) / 64), static_cast<unsigned>(tb));
     if (x_dtype == TAGG_DTYPE_BF16)

@@ -1,5 +1,6 @@
 """Small invocations of every product kernel, for compute-sanitizer (memcheck / racecheck /
 synccheck): python tools/sanitize.py"""
+import os
 import sys
 
 import numpy as np
@@ -21,9 +22,11 @@ bsc = np.stack([b[3] for b in bs])
 a, sa = torch.from_numpy(ac).to(dev), torch.from_numpy(asc).to(dev)
 b, sb = torch.from_numpy(bc).to(dev), torch.from_numpy(bsc).to(dev)
 gs = torch.tensor(sizes, dtype=torch.int32, device=dev)
-for tile in ("pair_n256", "pair_n128", "1cta"):
-    for exact in (False, True):
-        tg.grouped_gemm_fp8(a, sa, b, sb, gs, tile=tile, exact_promotion=exact)
+PART = os.environ.get("SANITIZE_PART", "all")  # diagnostics: run one piece (base / bidx / flag / overlap)
+if PART in ("all", "base"):
+    for tile in ("pair_n256", "pair_n128", "1cta"):
+        for exact in (False, True):
+            tg.grouped_gemm_fp8(a, sa, b, sb, gs, tile=tile, exact_promotion=exact)
 # exact-size output: any store past sum(M_g) would be out of bounds
 out = torch.empty((m, n), dtype=torch.bfloat16, device=dev)
 tg.grouped_gemm_fp8(a[:m].contiguous(), sa[:m].contiguous(), b, sb, gs, out=out)
@@ -43,12 +46,19 @@ idx = torch.randperm(m, device=dev).to(torch.int32)
 tg.quantize_col_blocks(xb, gs, index=idx, row_weights=torch.rand(m, device=dev))
 # groups sharing experts (b_index), the device error flag, a PDL-overlap chain into one output
 bi = torch.tensor([1, 0, 2, 1, 5, 3], dtype=torch.int32, device=dev)
-tg.grouped_gemm_fp8(a, sa, b, sb, gs, b_index=bi, check=True)
-flag = torch.zeros(1, dtype=torch.int32, device=dev)
-tg.grouped_gemm_fp8(a, sa, b, sb, torch.tensor([5000, 1, 0, 0, 0, 0], dtype=torch.int32, device=dev),
-                    err_flag=flag)
-for _ in range(3):
-    tg.grouped_gemm_fp8(a, sa, b, sb, gs, out=out[:m] if False else None, pdl_overlap=True)
+if PART in ("all", "bidx"):
+    tg.grouped_gemm_fp8(a, sa, b, sb, gs, b_index=bi, check=True)
+if PART in ("all", "flag"):
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    tg.grouped_gemm_fp8(a, sa, b, sb, torch.tensor([5000, 1, 0, 0, 0, 0], dtype=torch.int32, device=dev),
+                        err_flag=flag)
+if PART in ("all", "overlap"):
+    for _ in range(3):
+        tg.grouped_gemm_fp8(a, sa, b, sb, gs, pdl_overlap=True)
+if PART == "overlap_sync":  # the same launches with a device sync between them: no grid overlap
+    for _ in range(3):
+        tg.grouped_gemm_fp8(a, sa, b, sb, gs, pdl_overlap=True)
+        torch.cuda.synchronize()
 from paper_2508_16584_b200 import moe  # noqa: E402
 
 h = torch.randn((m + 40, 512), device=dev).to(torch.bfloat16)
