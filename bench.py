@@ -591,6 +591,8 @@ def main():
 
     e2e_ms = _timed_steps(torch, dist, world, e2e_step, half, 1) / half
     e2e_val = world * flops_step / (e2e_ms * 1e-3) / 1e12
+    # the host link bounds it: PCIe is full duplex, so the larger direction sets the time
+    e2e_link_gbs = max(h2d, d2h) / (e2e_ms * 1e-3) / 1e9
 
     # ---------------------------------------------------------------- CPU baseline + self-check (rank 0, N=1)
     cpu = None
@@ -665,6 +667,7 @@ def main():
                      "traffic_source": "profiles/traffic_residual_sweep.json (ncu launch list, mean per launch)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "bound": "host link (PCIe)", "busier_direction_gbs": e2e_link_gbs,
                 "note": "127 independent host-buffer calls per step: each copies its own A rows, A scales and group "
                         "sizes H2D (pinned) and its C rows D2H; expert weights resident; copies overlap the GEMMs "
                         "(hostpipe.run_host_batches)"},
