@@ -290,6 +290,16 @@ def pipelined_expert_gemm(a_codes: torch.Tensor, a_scales: torch.Tensor, expert_
     rows, k = a_codes.shape
     kb = a_scales.shape[1]
     dev = a_codes.device
+    if plan is None and chunks == 1 and in_place:
+        # one chunk has nothing to overlap: the sequential in-place exchange, without the
+        # chunk plan's bookkeeping and the packed-row copy
+        a_loc, sa_loc, meta = dispatch(a_codes, a_scales, expert_ids.reshape(-1), num_experts, group, in_place=True)
+        out = torch.empty((a_loc.shape[0], n_out), dtype=out_dtype, device=dev)
+        if a_loc.shape[0]:
+            y = expert_gemm(a_loc, sa_loc, meta.group_sizes, b_index=meta.b_index, out=out)
+            if y.data_ptr() != out.data_ptr():
+                out.copy_(y[:a_loc.shape[0]])
+        return combine(out, meta, group)
     if plan is None:
         plan = plan_chunks(expert_ids, num_experts, chunks, group)
     width = -(-(k + 4 * kb) // 16) * 16     # 16-byte rows: the GEMM's TMA reads codes in place

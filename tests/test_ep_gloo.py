@@ -138,7 +138,7 @@ def _pipeline_worker(rank, world, port, rows_per_rank, k, experts, chunks, seed,
 
 
 @pytest.mark.parametrize("in_place", [True, False])
-@pytest.mark.parametrize("rows_per_rank,experts,chunks", [((300, 170), 8, 3), ((1, 0), 4, 2), ((3, 2), 4, 5)])
+@pytest.mark.parametrize("rows_per_rank,experts,chunks", [((300, 170), 8, 3), ((1, 0), 4, 2), ((3, 2), 4, 5), ((257, 90), 8, 1)])
 def test_pipelined_expert_gemm_world2(rows_per_rank, experts, chunks, in_place):
     """Chunked dispatch -> expert GEMM -> combine returns every row's result home, in order."""
     ctx = mp.get_context("spawn")
