@@ -232,6 +232,21 @@ int tagg_quantize_col_blocks_gather(const void* x, int x_dtype, int64_t ldx, con
  */
 int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, const float* sdy, int64_t m_alloc,
                    const int32_t* group_sizes, int G, int K, int N, void* dw, void* stream);
+/* The same with flags.  TAGG_WGRAD_DY_BLOCK128: the caller asserts sdy is constant over every
+   128-column block of each token block (dY quantized with tagg_quantize_col_blocks_ex, block_cols
+   = 128, the reference's 128x128 block recipe fp8.py:154-176 per group token block).  The
+   promotion then uses one scale per drained 128-column half: one FFMA2 per element pair instead of
+   an FMUL2 and an FFMA2. */
+#define TAGG_WGRAD_DY_BLOCK128 1u
+int tagg_wgrad_fp8_ex(const void* x, const float* sx, const void* dy, const float* sdy, int64_t m_alloc,
+                      const int32_t* group_sizes, int G, int K, int N, void* dw, uint32_t flags, void* stream);
+/* Column-block quantization with a row gather (index / row_weights nullable, as above) and a block
+   width: block_cols = 1 is tagg_quantize_col_blocks(_gather); block_cols = 128 takes one amax per
+   (token block, 128 columns) and writes it to all 128 columns' scale slots (cols % 128 == 0). */
+int tagg_quantize_col_blocks_ex(const void* x, int x_dtype, int64_t ldx, const int32_t* index,
+                                const float* row_weights, int64_t rows, int cols, const int32_t* group_sizes, int G,
+                                void* codes, int64_t ldc, float* scales, int32_t* err_flag, int block_cols,
+                                void* stream);
 
 /* ---- host planners (no GPU needed) ---- */
 /* ProblemConfig validation (engine.py:77-92). */

@@ -100,12 +100,15 @@ def bf16_bits_to_f32(bits) -> np.ndarray:
     return u.view(np.float32)
 
 
-def quantize_col_blocks(x, group_sizes):
+def quantize_col_blocks(x, group_sizes, block_cols: int = 1):
     """Per-group 128x1 quantization for the weight gradient (the ragged token axis is the
     reduction axis): for each group and each of its 128-token blocks, one scale per
     column, s = fl(amax / 448) (1.0 when zero), codes = encode(fl(x / s)) -- the
     fp8.py:132-151 recipe applied down the columns of each block.  Returns
     (codes [M, C], scales [TB, C]) with TB = sum(ceil(M_g / 128)) rows, group by group.
+    block_cols = 128: one scale per (token block, 128 columns), the 128x128 block recipe of
+    fp8.py:154-176 (quantize_blocks) applied per group token block, repeated in each of the
+    block's 128 column slots.
     """
     x = np.ascontiguousarray(x, dtype=np.float32)
     rows, cols = x.shape
@@ -117,6 +120,8 @@ def quantize_col_blocks(x, group_sizes):
         for b0 in range(0, m, SCALE_BLOCK):
             sl = slice(off + b0, off + min(b0 + SCALE_BLOCK, m))
             amax = np.abs(x[sl]).max(axis=0)
+            if block_cols == 128:
+                amax = np.repeat(amax.reshape(-1, 128).max(axis=1), 128)
             s = np.where(amax > 0, amax / np.float32(E4M3_MAX), np.float32(1.0)).astype(np.float32)
             blocks.append(s)
             codes[sl] = encode(x[sl] / s[None, :])

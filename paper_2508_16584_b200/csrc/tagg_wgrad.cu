@@ -67,6 +67,11 @@ __device__ __forceinline__ void wg_stamp(unsigned long long* tr, int ev, uint32_
 // CTA pair (cluster of 2, tcgen05 cta_group::2) per 256 (K) x 256 (N) tile of dW_g: CTA
 // `rank` holds K rows [k0 + 128 rank, +128) of X^T and B columns [n0 + 128 rank, +128)
 // of dY; each CTA's TMEM gets its 128 rows x all 256 columns.
+// kDyBlock: sdy is constant over every 128-column block of a token block (the 128x128 dY recipe of
+// tagg_quantize_col_blocks_ex, block_cols = 128): a thread's 128 columns are one block, so its
+// promotion is s = fl(sx * sdy) once per token block and one FFMA2 per element pair -- the forward
+// kernel's promotion -- instead of an FMUL2 and an FFMA2.
+template <bool kDyBlock>
 __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -263,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
         const uint32_t slot = sS0 + sring * kScaleSlot;
         const float sxk = ld_shared_f32(slot + 4u * r);
         const uint32_t sdy = slot + 512u + 4u * (128u * half);
+        const float sblk = kDyBlock ? __fmul_rn(sxk, ld_shared_f32(sdy)) : 0.0f;
         mbar_wait_addr(tfull0 + 8 * acc_i, accph);
         if (tr) wg_stamp(p.trace, kWgPromoFull, kiter);
         tc_fence_after();
@@ -277,6 +283,13 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
             __syncwarp();
             if (lane == 0) mbar_arrive_leader_addr(tempty0 + 8 * acc_i);
             if (tr) wg_stamp(p.trace, kWgPromoFreed, kiter);
+          }
+          if constexpr (kDyBlock) {
+            // acc = fl(acc + inner * s), s = fl(sx * sdy): one FFMA2 per pair, as in the forward
+#pragma unroll
+            for (int c = 0; c < 64; c += 2)
+              ffma2(acc[64 * c2 + c], acc[64 * c2 + c + 1], __uint_as_float(v[c]), __uint_as_float(v[c + 1]), sblk);
+            continue;
           }
 #pragma unroll
           for (int c = 0; c < 64; c += 4) {
@@ -420,7 +433,10 @@ __global__ void __launch_bounds__(128) quantize_col_blocks_kernel(const void* __
 
 // Vector form: thread = 8 consecutive columns (16-B bf16 / 32-B f32 loads, 8-B code stores),
 // 64 threads = 512 columns per CTA; the (group, token block) lookup is the same table walk.
-template <bool kBf16>
+// kBlock128: one scale per (token block, 128 columns) -- the reference's 128x128 block recipe
+// (fp8.py:154-176) applied to each group's token blocks -- written to all 128 columns' scale
+// slots, so the wgrad can promote with one scale per drained 128-column half (1 op per pair).
+template <bool kBf16, bool kBlock128 = false>
 // Optional gather: grouped row r reads row_weights[r] * x[index[r]] (index / row_weights
 // nullable), so token-ordered activations are quantized into the grouped layout without a copy.
 __global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* __restrict__ x, int64_t ldx, int cols,
@@ -466,6 +482,7 @@ __global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* 
   if (rows <= 0) return;
   const int64_t row0 = s_row0;
   const int c0 = (blockIdx.x * 64 + threadIdx.x) * 8;
+  // kBlock128: cols % 128 == 0, so the 16 lanes of a 128-column block are all in or all out
   if (c0 >= cols) return;  // cols % 8 == 0 on this path
   auto load8 = [&](int64_t r_grouped, float (&v)[8]) {
     const int64_t rr = index ? static_cast<int64_t>(index[r_grouped]) : r_grouped;
@@ -502,6 +519,16 @@ __global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* 
       bad |= !(m <= 3.402823466e38f);
       amax[j] = fmaxf(amax[j], m);
     }
+  }
+  if constexpr (kBlock128) {
+    float bm = amax[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) bm = fmaxf(bm, amax[j]);
+    const unsigned half_mask = 0xFFFFu << (threadIdx.x & 16);  // this 128-column block's 16 lanes
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(half_mask, bm, o));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) amax[j] = bm;
   }
   float s[8];
 #pragma unroll
@@ -540,7 +567,8 @@ extern "C" int64_t tagg_token_blocks_bound(int64_t m_alloc, int G) {
 
 static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
                                     const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
-                                    int32_t* err_flag, const int32_t* index, const float* row_weights, void* stream);
+                                    int32_t* err_flag, const int32_t* index, const float* row_weights, void* stream,
+                                    int block_cols = 1);
 
 extern "C" int tagg_quantize_col_blocks(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
                                         const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
@@ -561,9 +589,25 @@ extern "C" int tagg_quantize_col_blocks_gather(const void* x, int x_dtype, int64
                                   row_weights, stream);
 }
 
+extern "C" int tagg_quantize_col_blocks_ex(const void* x, int x_dtype, int64_t ldx, const int32_t* index,
+                                           const float* row_weights, int64_t rows, int cols,
+                                           const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
+                                           int32_t* err_flag, int block_cols, void* stream) {
+  if (block_cols != 1 && block_cols != 128) return TAGG_ERR_CONFIG;
+  if (block_cols == 128 && (cols % 128 || (reinterpret_cast<uintptr_t>(x) % 16) ||
+                            ((ldx * (x_dtype == TAGG_DTYPE_BF16 ? 2 : 4)) % 16) ||
+                            (reinterpret_cast<uintptr_t>(codes) % 8) || (ldc % 8) ||
+                            (reinterpret_cast<uintptr_t>(scales) % 16)))
+    return TAGG_ERR_ALIGNMENT;  // the 128-column block form is the vector kernel only
+  if (rows > 0 && index == nullptr && row_weights != nullptr) return TAGG_ERR_SHAPE;
+  return quantize_col_blocks_impl(x, x_dtype, rows, cols, ldx, group_sizes, G, codes, ldc, scales, err_flag, index,
+                                  row_weights, stream, block_cols);
+}
+
 static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
                                     const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
-                                    int32_t* err_flag, const int32_t* index, const float* row_weights, void* stream) {
+                                    int32_t* err_flag, const int32_t* index, const float* row_weights, void* stream,
+                                    int block_cols) {
   if (x_dtype != TAGG_DTYPE_BF16 && x_dtype != TAGG_DTYPE_F32) return TAGG_ERR_CONFIG;
   if (G < 1 || cols < 1 || m_alloc < 0 || ldx < cols || ldc < cols) return TAGG_ERR_SHAPE;
   if (m_alloc == 0) return TAGG_OK;
@@ -574,6 +618,16 @@ static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc,
   const int esz = x_dtype == TAGG_DTYPE_BF16 ? 2 : 4;
   const bool v8 = cols % 8 == 0 && !(reinterpret_cast<uintptr_t>(x) % 16) && !((ldx * esz) % 16) &&
                   !(reinterpret_cast<uintptr_t>(codes) % 8) && !(ldc % 8) && !(reinterpret_cast<uintptr_t>(scales) % 16);
+  if (v8 && block_cols == 128) {
+    const dim3 g8(static_cast<unsigned>((cols / 8 + 63) / 64), static_cast<unsigned>(tb));
+    if (x_dtype == TAGG_DTYPE_BF16)
+      wg::quantize_col_blocks_v8_kernel<true, true><<<g8, 64, 0, st>>>(
+          x, ldx, cols, group_sizes, G, static_cast<uint8_t*>(codes), ldc, scales, err_flag, index, row_weights);
+    else
+      wg::quantize_col_blocks_v8_kernel<false, true><<<g8, 64, 0, st>>>(
+          x, ldx, cols, group_sizes, G, static_cast<uint8_t*>(codes), ldc, scales, err_flag, index, row_weights);
+    return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
+  }
   if (v8) {
     const dim3 g8(static_cast<unsigned>((cols / 8 + 63) / 64), static_cast<unsigned>(tb));
     if (x_dtype == TAGG_DTYPE_BF16)
@@ -598,6 +652,12 @@ static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc,
 
 extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, const float* sdy, int64_t m_alloc,
                               const int32_t* group_sizes, int G, int K, int N, void* dw, void* stream) {
+  return tagg_wgrad_fp8_ex(x, sx, dy, sdy, m_alloc, group_sizes, G, K, N, dw, 0u, stream);
+}
+
+extern "C" int tagg_wgrad_fp8_ex(const void* x, const float* sx, const void* dy, const float* sdy, int64_t m_alloc,
+                                 const int32_t* group_sizes, int G, int K, int N, void* dw, uint32_t flags,
+                                 void* stream) {
   using namespace tagg::wg;
   if (G < 1 || K < 128 || N < 128 || K % 128 || N % 128) return TAGG_ERR_CONFIG;
   if (m_alloc < 0) return TAGG_ERR_SHAPE;
@@ -645,11 +705,13 @@ extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, co
   p.off_bar = p.off_tab + tab;
   const uint32_t smem = p.off_bar + (2 * kStages + 2 * kNumAcc + 2 * kScaleRing) * 8 + 16 + 1024;
   if (smem > 232448) return TAGG_ERR_UNSUPPORTED;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448) != cudaSuccess)
+  const bool dy_block = (flags & TAGG_WGRAD_DY_BLOCK128) != 0;
+  auto kern = dy_block ? wgrad_kernel<true> : wgrad_kernel<false>;
+  static bool configured[2] = {false, false};
+  if (!configured[dy_block]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448) != cudaSuccess)
       return TAGG_ERR_CUDA;
-    configured = true;
+    configured[dy_block] = true;
   }
   const int64_t tiles = static_cast<int64_t>(G) * p.KT * p.NT;
   const int grid = static_cast<int>(std::min<int64_t>(sms / 2, tiles)) * 2;
@@ -665,7 +727,7 @@ extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, co
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_kernel, p);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
   if (e != cudaSuccess) {
     std::fprintf(stderr, "tagg_wgrad_fp8: launch failed: %s\n", cudaGetErrorString(e));
     return TAGG_ERR_CUDA;

@@ -17,14 +17,22 @@ from .quant import _DTYPES, _check_cuda, _stream
 
 
 def quantize_col_blocks(x: torch.Tensor, group_sizes: torch.Tensor, *, check: bool = False,
-                        index: torch.Tensor | None = None, row_weights: torch.Tensor | None = None):
+                        index: torch.Tensor | None = None, row_weights: torch.Tensor | None = None,
+                        block_cols: int = 1):
     """(codes uint8 [M, C], scales f32 [TB_bound, C]) for x [M, C] in the grouped layout.
 
     Scale row tb holds the tb-th (group, 128-token block) in group order; only the first
     sum(ceil(M_g/128)) rows are defined (group sizes stay on the device: no host sync).
     With ``index`` (int [M]), grouped row r is ``row_weights[r] * x[index[r]]`` (weights
     optional): token-ordered rows are quantized into the grouped layout without a copy.
+    ``block_cols=128``: one scale per (token block, 128 columns) -- the 128x128 block recipe
+    of fp8.py:154-176 per group token block -- repeated in its 128 columns' slots; a dY
+    quantized this way lets ``wgrad_fp8(..., dy_block128=True)`` promote with one op per pair.
     """
+    if block_cols == 128:
+        return _quantize_col_blocks_ex(x, group_sizes, index, row_weights, check, 128)
+    if block_cols != 1:
+        raise InvalidInput("block_cols must be 1 or 128")
     if index is not None:
         return _quantize_col_blocks_gather(x, group_sizes, index, row_weights, check)
     _check_cuda(x, "x")
@@ -73,8 +81,34 @@ def _quantize_col_blocks_gather(x, group_sizes, index, row_weights, check):
     return codes, scales
 
 
-def wgrad_fp8(x_codes, x_scales, dy_codes, dy_scales, group_sizes, out=None) -> torch.Tensor:
-    """dW [G, K, N] bf16 = X_g^T dY_g per group (K, N multiples of 128)."""
+def _quantize_col_blocks_ex(x, group_sizes, index, row_weights, check, block_cols):
+    _check_cuda(x, "x")
+    if x.dim() != 2 or x.dtype not in _DTYPES or x.stride(1) != 1:
+        raise ShapeMismatch("x must be a row-major bf16 / f32 matrix")
+    if group_sizes.dtype != torch.int32 or not group_sizes.is_cuda:
+        raise ShapeMismatch("group_sizes must be an int32 CUDA tensor")
+    idx = None if index is None else index.to(torch.int32).contiguous()
+    w = None if row_weights is None else row_weights.to(torch.float32).contiguous()
+    m, c = (x.shape[0] if idx is None else idx.numel()), x.shape[1]
+    g = group_sizes.numel()
+    tb = lib().tagg_token_blocks_bound(m, g)
+    codes = torch.empty((m, c), dtype=torch.uint8, device=x.device)
+    scales = torch.empty((max(tb, 1), c), dtype=torch.float32, device=x.device)
+    err = torch.zeros(1, dtype=torch.int32, device=x.device)
+    rc = lib().tagg_quantize_col_blocks_ex(x.data_ptr(), _DTYPES[x.dtype], x.stride(0),
+                                           None if idx is None else idx.data_ptr(), None if w is None else w.data_ptr(),
+                                           m, c, group_sizes.data_ptr(), g, codes.data_ptr(), c, scales.data_ptr(),
+                                           err.data_ptr(), block_cols, _stream())
+    raise_for_status(rc, "tagg_quantize_col_blocks_ex")
+    if check and int(err.item()):
+        raise InvalidInput("matrix entries must be finite")
+    return codes, scales
+
+
+def wgrad_fp8(x_codes, x_scales, dy_codes, dy_scales, group_sizes, out=None, *, dy_block128=False) -> torch.Tensor:
+    """dW [G, K, N] bf16 = X_g^T dY_g per group (K, N multiples of 128).  ``dy_block128``: dY's
+    scales are constant per 128 columns (quantize_col_blocks(..., block_cols=128)); the promotion
+    then takes one FFMA2 per element pair (TAGG_WGRAD_DY_BLOCK128)."""
     for t, what in ((x_codes, "x_codes"), (dy_codes, "dy_codes")):
         _check_cuda(t, what)
     if x_codes.dtype == torch.float8_e4m3fn:
@@ -103,7 +137,7 @@ def wgrad_fp8(x_codes, x_scales, dy_codes, dy_scales, group_sizes, out=None) -> 
     if (out.dtype not in (torch.bfloat16, torch.int16, torch.uint16) or tuple(out.shape) != (g, k, n)
             or not out.is_contiguous() or out.device != x_codes.device):
         raise ShapeMismatch(f"out must be a contiguous bf16 [{g}, {k}, {n}] tensor on the operands' device")
-    rc = lib().tagg_wgrad_fp8(x_codes.data_ptr(), x_scales.data_ptr(), dy_codes.data_ptr(), dy_scales.data_ptr(), m,
-                              group_sizes.data_ptr(), g, k, n, out.data_ptr(), _stream())
+    rc = lib().tagg_wgrad_fp8_ex(x_codes.data_ptr(), x_scales.data_ptr(), dy_codes.data_ptr(), dy_scales.data_ptr(),
+                                 m, group_sizes.data_ptr(), g, k, n, out.data_ptr(), 1 if dy_block128 else 0, _stream())
     raise_for_status(rc, "tagg_wgrad_fp8")
     return out

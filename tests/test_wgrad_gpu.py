@@ -103,3 +103,54 @@ def test_col_block_gather_equals_quantizing_the_gathered_copy(dtype):
     plain_c, plain_s = tg.quantize_col_blocks(x, gs, index=idx)
     want_pc, want_ps = tg.quantize_col_blocks(x.index_select(0, idx.long()).contiguous(), gs)
     assert torch.equal(plain_c, want_pc) and torch.equal(plain_s[:tb], want_ps[:tb])
+
+
+@pytest.mark.parametrize("sizes", [(200,), (1, 0, 129, 255, 384)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("gather", [False, True])
+def test_quantize_col_blocks_128_column_blocks_is_bit_exact(sizes, dtype, gather):
+    """block_cols=128: one scale per (group token block, 128 columns), the 128x128 block recipe
+    of fp8.py:154-176, against oracle/fp8.quantize_col_blocks(block_cols=128)."""
+    x, _ = _data(sizes, 384, 256, 2)
+    m = sum(sizes)
+    xt = torch.from_numpy(x).to(DEV).to(dtype)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    if gather:
+        perm = torch.randperm(m, generator=torch.Generator().manual_seed(m)).to(torch.int32)
+        w = torch.rand(m, generator=torch.Generator().manual_seed(m + 1))
+        src = torch.empty_like(xt)
+        src[perm.to(torch.int64).to(DEV)] = xt  # token order: grouped row r = w[r] * src[perm[r]]
+        codes, scales = tg.quantize_col_blocks(src, gs, index=perm.to(DEV), row_weights=w.to(DEV), block_cols=128,
+                                               check=True)
+        ref = (w.numpy()[:, None] * xt.float().cpu().numpy()).astype(np.float32)
+    else:
+        codes, scales = tg.quantize_col_blocks(xt, gs, block_cols=128, check=True)
+        ref = xt.float().cpu().numpy()
+    torch.cuda.synchronize()
+    want_c, want_s = ofp8.quantize_col_blocks(ref, sizes, block_cols=128)
+    np.testing.assert_array_equal(codes.cpu().numpy(), want_c)
+    tb = want_s.shape[0]
+    np.testing.assert_array_equal(scales[:tb].cpu().numpy().view(np.uint32), want_s.view(np.uint32))
+
+
+@pytest.mark.parametrize("sizes,k,n", [
+    ((300, 0, 1, 77, 256), 256, 384),
+    (tuple(range(1, 128, 9)), 128, 256),
+    ((1000, 513), 384, 256),
+])
+def test_wgrad_dy_block128_matches_oracle(sizes, k, n):
+    """TAGG_WGRAD_DY_BLOCK128 (dY with 128x128 block scales, one FFMA2 per pair) against the
+    C oracle on the same operands (the oracle reads the per-column scale slots, which repeat
+    the block scale)."""
+    x, dy = _data(sizes, k, n, sum(sizes) + 5)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    xc, xs = tg.quantize_col_blocks(torch.from_numpy(x).to(DEV), gs)
+    dc, ds = tg.quantize_col_blocks(torch.from_numpy(dy).to(DEV), gs, block_cols=128)
+    dw = tg.wgrad_fp8(xc, xs, dc, ds, gs, dy_block128=True)
+    torch.cuda.synchronize()
+    tb = sum(-(-s // 128) for s in sizes)
+    want = orc.wgrad(xc.cpu().numpy(), xs[:tb].cpu().numpy(), dc.cpu().numpy(), ds[:tb].cpu().numpy(), sizes,
+                     threads=8)
+    got = dw.view(torch.int16).cpu().numpy().view(np.uint16)
+    for g in range(len(sizes)):
+        assert_parity(got[g], want[g], label=f"group {g}")
