@@ -39,9 +39,9 @@ extern "C" {
 #define TAGG_ERR_ALIGNMENT (-5)         /* AlignmentError       errors.py:30-40 */
 #define TAGG_ERR_NO_ALIGNED_SOLUTION (-6) /* NoAlignedSolution  errors.py:64-68 */
 #define TAGG_ERR_RES_OUT_OF_RANGE (-7)  /* ResOutOfRange        errors.py:60 */
-#define TAGG_ERR_UNSUPPORTED (-8)       /* shape exceeds this build's on-chip budget: any K <= 15872
-                                           fits (two S_A windows + two stages in 227 KB of smem; 16128
-                                           is the largest K that does),
+#define TAGG_ERR_UNSUPPORTED (-8)       /* shape exceeds this build's on-chip budget: K <= 16384
+                                           (128 k-blocks of S_B staging; the S_A window drops to one
+                                           slot when two do not fit beside two pipeline stages),
                                            G up to ~8k (device group tables in smem), M < 2^31 */
 #define TAGG_ERR_CUDA (-9)              /* CUDA runtime / driver failure */
 

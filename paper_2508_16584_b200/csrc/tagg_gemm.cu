@@ -90,6 +90,7 @@ struct Params {
   int64_t sb_sg, sb_skb, sb_snb;
   int32_t G, N, K, kb_count, n_tiles, sa_rb, b_kmajor, b_shared, b_experts;
   uint32_t stages, sa_buf_bytes;
+  uint32_t sa_slots;    // S_A / S_B window buffers: 2, or 1 when that frees a pipeline stage
   uint32_t epi_passes;  // 256-column tiles: 1 = 64 KB staging, all 4 chunks at once; 2 = 32 KB, two passes
   uint32_t off_a, off_b, off_c, off_sa, off_sb, off_tab, off_bar;
   uint32_t dbg;
@@ -213,6 +214,56 @@ __device__ __forceinline__ int sa_row_prev(int64_t row0, int rb) {
   return rp;
 }
 
+// A promotion warp is done reading the tile's scale window: one arrive per warp (the
+// barrier counts kNumPromoWarps), after the k-loop.  (Handing it back at the last read, two
+// k-blocks earlier, measured 2-3% more cycles.)  The reads are ordinary ld.shared; the arrive
+// (release) orders them before the scale loader's next async-proxy writes into the slot.
+__device__ __forceinline__ void release_window(uint32_t bar, int lane) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive_addr(bar);
+}
+
+// One tile's scales into window slot `slot`: its S_B columns (4-byte cp.async by all 32 lanes)
+// and its S_A over-fetch window (one 1-D bulk copy by lane 0, prefetch.py:50-72), both
+// tracked by safull[slot].
+__device__ __forceinline__ void load_scale_window(const Params& p, const Tile& T, int gb, uint32_t slot,
+                                                  uint32_t sfull0, uint32_t sSA0, uint32_t sSB0, uint8_t* sSA,
+                                                  int kbc, int rb, int lane) {
+  const uint32_t sab = slot;
+  // ---- S_B columns of the tile (engine.py:166-169: column block n // 128)
+  {
+    const float* sbg = p.sb + static_cast<int64_t>(gb) * p.sb_sg;
+    const uint32_t dst0 = sSB0 + sab * kSbBufBytes;
+#pragma unroll
+    for (int c = 0; c < kSbCols; ++c) {
+      // a column block past N (the right half of an edge tile) repeats the last valid one:
+      // every slot is rewritten each tile, so the promotion never reads a stale slot
+      const int nb = min((T.n0 >> 7) + c, (p.N - 1) >> 7);
+      for (int kb = lane; kb < kbc; kb += 32)
+        cp_async_4(dst0 + 4u * (c * kbc + kb), sbg + static_cast<int64_t>(kb) * p.sb_skb +
+                                                   static_cast<int64_t>(nb) * p.sb_snb);
+    }
+    cp_async_mbar_arrive_noinc(sfull0 + 8 * sab);
+  }
+  // ---- S_A over-fetch window (prefetch.py:50-72)
+  if (lane == 0) {
+    const int rp = sa_row_prev(T.row0, rb);
+    const int64_t start_row = static_cast<int64_t>(T.row0) - rp;
+    const int64_t want = ((static_cast<int64_t>(rp + BM) * rb) + 15) & ~int64_t(15);
+    int64_t avail = (p.m_alloc - start_row) * rb;
+    if (avail < 0) avail = 0;
+    const int64_t lim = min(want, avail);
+    const uint32_t bulk = static_cast<uint32_t>(lim & ~int64_t(15));
+    const uint32_t tail = static_cast<uint32_t>(lim) - bulk;
+    uint8_t* dst = sSA + sab * p.sa_buf_bytes;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(p.sa) + start_row * rb;
+    for (uint32_t i = 0; i < tail; i += 4)  // < 16 B at the very end of S_A
+      *reinterpret_cast<float*>(dst + bulk + i) = __ldg(reinterpret_cast<const float*>(src + bulk + i));
+    mbar_arrive_expect_tx_addr(sfull0 + 8 * sab, bulk);
+    if (bulk) bulk_load_1d_addr(sSA0 + sab * p.sa_buf_bytes, src, bulk, sfull0 + 8 * sab);
+  }
+}
+
 // The persistent grid's cluster count, re-read from %nctaid per use: kept live across the
 // tile loops in the 72-register control warps it was spilled to local memory.
 template <int kCG>
@@ -277,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       mbar_init(&tempty[i], kNumPromoWarps * kCG);     // promotion warps of every CTA in the pair
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&safull[i], 1 + 32);  // S_A bulk copy (expect_tx) + 32 producer lanes' S_B cp.async
+      mbar_init(&safull[i], 1 + 32);  // S_A bulk copy (expect_tx) + 32 scale-loader lanes' S_B cp.async
       mbar_init(&saempty[i], kNumPromoWarps);
     }
     fence_mbar_init();
@@ -363,52 +414,16 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
    const int total_tiles = ld_shared_s32(smem_u32(&tab_tile[G]));
    if (warp == 0) {
     // ========================================================== TMA producer
-    // Per tile: the S_A over-fetch window (one 1-D bulk copy by lane 0) and this tile's
-    // S_B columns (4-byte cp.async by all 32 lanes, tracked by the same barrier), then
-    // the A / B k-blocks (lane 0).
-    uint32_t stage = 0, phase = 0, sab = 0, saph = 0, kiter = 0;
-    const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
+    // Per tile: the A / B k-blocks (one elected lane issues).  The tile's scales are loaded
+    // by warp 2 (below), so this loop never waits on the promotion's scale window
+    // (measured 1-2% fewer cycles than loading them here).
+    uint32_t stage = 0, phase = 0, kiter = 0;
     const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
     const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
-    const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
     const int xs = tail_split_count(total_tiles, grid_clusters<kCG>(), C::kHalfTiles);
     for (int t = cluster_index<kCG>(); t < total_tiles + xs; t += grid_clusters<kCG>()) {
       const Tile T = decode_unit<kCG, kBN>(t, total_tiles, xs, rank, tab_tile, tab_row, tab_size, tab_crow, G);
       const int gb = ld_shared_s32(smem_u32(&tab_bidx[T.g]));
-      mbar_wait_addr(sempty0 + 8 * sab, saph ^ 1);
-      // ---- S_B columns of the tile (engine.py:166-169: column block n // 128)
-      {
-        const float* sbg = p.sb + static_cast<int64_t>(gb) * p.sb_sg;
-        const uint32_t dst0 = sSB0 + sab * kSbBufBytes;
-#pragma unroll
-        for (int c = 0; c < kSbCols; ++c) {
-          // a column block past N (the right half of an edge tile) repeats the last valid one:
-          // every slot is rewritten each tile, so the promotion never reads a stale slot
-          const int nb = min((T.n0 >> 7) + c, (p.N - 1) >> 7);
-          for (int kb = lane; kb < kbc; kb += 32)
-            cp_async_4(dst0 + 4u * (c * kbc + kb), sbg + static_cast<int64_t>(kb) * p.sb_skb +
-                                                       static_cast<int64_t>(nb) * p.sb_snb);
-        }
-        cp_async_mbar_arrive_noinc(sfull0 + 8 * sab);
-      }
-      // ---- S_A over-fetch window (prefetch.py:50-72)
-      if (lane == 0) {
-        const int rp = sa_row_prev(T.row0, rb);
-        const int64_t start_row = static_cast<int64_t>(T.row0) - rp;
-        const int64_t want = ((static_cast<int64_t>(rp + BM) * rb) + 15) & ~int64_t(15);
-        int64_t avail = (p.m_alloc - start_row) * rb;
-        if (avail < 0) avail = 0;
-        const int64_t lim = min(want, avail);
-        const uint32_t bulk = static_cast<uint32_t>(lim & ~int64_t(15));
-        const uint32_t tail = static_cast<uint32_t>(lim) - bulk;
-        uint8_t* dst = sSA + sab * p.sa_buf_bytes;
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.sa) + start_row * rb;
-        for (uint32_t i = 0; i < tail; i += 4)  // < 16 B at the very end of S_A
-          *reinterpret_cast<float*>(dst + bulk + i) = __ldg(reinterpret_cast<const float*>(src + bulk + i));
-        mbar_arrive_expect_tx_addr(sfull0 + 8 * sab, bulk);
-        if (bulk) bulk_load_1d_addr(sSA0 + sab * p.sa_buf_bytes, src, bulk, sfull0 + 8 * sab);
-      }
-      if (++sab == 2) { sab = 0; saph ^= 1; }
       // ---- A / B k-blocks.  This CTA stages its 128 rows of A and its B column share;
       // completion is counted on the leader's barrier.  The whole warp runs the loop
       // (warp-uniform operands, no per-lane waterfall); one elected lane issues.
@@ -448,6 +463,25 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         mbar_wait_addr(empty0 + 8 * stage, phase ^ 1);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    // ========================================================== scale loader
+    // Per tile: the S_A over-fetch window (one 1-D bulk copy by lane 0, prefetch.py:50-72) and
+    // the tile's S_B columns (4-byte cp.async by all 32 lanes, tracked by the same barrier), into
+    // a ring of p.sa_slots windows.  With one slot the next tile's window loads while the
+    // promotion runs the tile's epilogue.
+    uint32_t sab = 0, saph = 0;
+    const uint32_t nslots = p.sa_slots;
+    const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
+    const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
+    const int xs = tail_split_count(total_tiles, grid_clusters<kCG>(), C::kHalfTiles);
+    for (int t = cluster_index<kCG>(); t < total_tiles + xs; t += grid_clusters<kCG>()) {
+      const Tile T = decode_unit<kCG, kBN>(t, total_tiles, xs, rank, tab_tile, tab_row, tab_size, tab_crow, G);
+      const int gb = ld_shared_s32(smem_u32(&tab_bidx[T.g]));
+      mbar_wait_addr(sempty0 + 8 * sab, saph ^ 1);
+      load_scale_window(p, T, gb, sab, sfull0, sSA0, sSB0, sSA, kbc, rb, lane);
+      if (++sab == nslots) { sab = 0; saph ^= 1; }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -578,9 +612,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           ++kiter;
           if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_addr(sempty0 + 8 * sab);
-        if (++sab == 2) { sab = 0; saph ^= 1; }
+        release_window(sempty0 + 8 * sab, lane);
+        if (++sab == p.sa_slots) { sab = 0; saph ^= 1; }
         // epilogue: one pass, 4 staging chunks of 64 rows x 64 columns (8 KB each); each
         // CTA stores its own <= 64 rows with the pool (64-row block plan, descriptors.py:95-106)
         const int lg = T.valid > 0 ? 31 - __clz(T.valid) : 0;
@@ -699,9 +732,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         ++kiter;
         if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_addr(sempty0 + 8 * sab);
-      if (++sab == 2) { sab = 0; saph ^= 1; }
+      release_window(sempty0 + 8 * sab, lane);
+      if (++sab == p.sa_slots) { sab = 0; saph ^= 1; }
 
       if (tr_a) trace_stamp(p.trace, kEvEpiStart, tiles_done);
       // ---- epilogue: bf16 -> swizzled smem staging (2 chunks of 64 columns)
@@ -964,18 +996,19 @@ int sm_count() { return num_sms_for_current_device(); }
 
 // Smem layout for a given stage count; returns total bytes (incl. alignment slack).
 static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_acc, uint32_t stage_bytes_b,
-                            uint32_t staging_bytes) {
+                            uint32_t staging_bytes, uint32_t sa_slots) {
   // row_prev < 16 / gcd(rb, 16): the residue class of row0*rb mod 16 has that period
   const int rp_max = 16 / gcd_int(rb, 16) - 1;
   const uint32_t sa_buf = align_up(static_cast<uint32_t>(((rp_max + BM) * rb + 15) & ~15), 128);
   p.stages = stages;
   p.sa_buf_bytes = sa_buf;
+  p.sa_slots = sa_slots;
   p.off_a = 0;
   p.off_b = stages * kStageBytesA;
   p.off_c = p.off_b + stages * stage_bytes_b;
   p.off_sa = p.off_c + staging_bytes;
-  p.off_sb = p.off_sa + 2 * sa_buf;
-  p.off_tab = p.off_sb + 2 * kSbBufBytes;
+  p.off_sb = p.off_sa + sa_slots * sa_buf;
+  p.off_tab = p.off_sb + sa_slots * kSbBufBytes;
   const uint32_t tab_bytes = align_up(4u * static_cast<uint32_t>(2 * (G + 1) + 3 * G), 16);
   p.off_bar = p.off_tab + tab_bytes;
   const uint32_t bar_bytes = (2 * stages + 2 * num_acc + 4) * 8 + 16;
@@ -1170,25 +1203,37 @@ extern "C" int tagg_grouped_gemm_fp8_ex(const void* a, int64_t lda, const float*
   static const int env_passes = [] { const char* e = std::getenv("TAGG_EPI_PASSES"); return e ? std::atoi(e) : 0; }();
   uint32_t stage_cap = (flags >> 12) & 0xFu;
   if (!stage_cap && env_stages > 0) stage_cap = static_cast<uint32_t>(env_stages);
-  uint32_t stages = stage_cap ? std::min<uint32_t>(stage_cap, kMaxStages) : kMaxStages;
+  const uint32_t max_stages = stage_cap ? std::min<uint32_t>(stage_cap, kMaxStages) : kMaxStages;
+  // diagnostics: TAGG_SA_SLOTS=1/2 forces the scale-window ring depth
+  static const int env_slots = [] { const char* e = std::getenv("TAGG_SA_SLOTS"); return e ? std::atoi(e) : 0; }();
+  // The deepest pipeline that fits, and with it the scale-window ring: two windows, or one
+  // when that buys a stage on long tiles (K >= 6144: the 28 KB S_A window of K = 7168 is a
+  // whole 32 KB stage; 3 -> 4 stages measured 2-6% fewer cycles on DeepSeek-V3 gate+up and
+  // 7-8% on the sweep).  On shorter tiles the next window, requested when the tile's k-loop
+  // ends, lands late often enough to cancel the stage (K = 4096), so two windows stay.
+  const bool one_slot_ok = kb_count >= 48;
+  auto fit = [&](uint32_t staging_bytes, uint32_t& slots) -> uint32_t {
+    uint32_t best = 0;
+    for (uint32_t sl = 2; sl >= 1; --sl) {
+      if (env_slots ? static_cast<uint32_t>(env_slots) != sl : (sl == 1 && !one_slot_ok)) continue;
+      uint32_t st = max_stages;
+      while (st >= 2 && smem_layout(p, st, G, rb, num_acc, stage_bytes_b, staging_bytes, sl) > 232448) --st;
+      if (st > best) { best = st; slots = sl; }
+    }
+    return best;
+  };
   // 256-column tiles: a 64 KB C staging (single-pass epilogue, whose TMA stores then
-  // overlap the next tile's k-loop) when that still leaves >= 3 pipeline stages
-  // (measured: 3 stages feed the MMA as well as 4); else 32 KB and two passes.
+  // overlap the next tile's k-loop) when that still leaves >= 3 pipeline stages; else 32 KB
+  // and two passes.
+  uint32_t slots = 2, stages = 0;
   p.epi_passes = 2;
   if (bn == 256 && env_passes != 2) {
-    uint32_t s1 = stages;
-    for (; s1 >= 3; --s1)
-      if (smem_layout(p, s1, G, rb, num_acc, stage_bytes_b, 2 * kCStagingBytes) <= 232448) break;
-    if (s1 >= 3) {
-      stages = s1;
-      p.epi_passes = 1;
-    }
+    stages = fit(2 * kCStagingBytes, slots);
+    if (stages >= 3) p.epi_passes = 1;
   }
+  if (p.epi_passes != 1) stages = fit(kCStagingBytes, slots);
   const uint32_t staging = p.epi_passes == 1 ? 2 * kCStagingBytes : kCStagingBytes;
-  for (; stages >= 2; --stages) {
-    smem_bytes = smem_layout(p, stages, G, rb, num_acc, stage_bytes_b, staging);
-    if (smem_bytes <= 232448) break;
-  }
+  if (stages >= 2) smem_bytes = smem_layout(p, stages, G, rb, num_acc, stage_bytes_b, staging, slots);
   if (stages < 2) return TAGG_ERR_UNSUPPORTED;
 
   // ---- tensor maps: A, B, and the C store pool (8 heights)

@@ -297,16 +297,15 @@ def test_tile_map_with_tall_groups_spanning_super_rows(max_sms):
 
 
 def test_largest_k_and_the_unsupported_limit():
-    """K is bounded by the on-chip budget (two S_A windows of 128 rows x 4*ceil(K/128) bytes
-    beside two pipeline stages): every K <= 15872 fits (16128 is the largest that does), and
-    K = 16256 raises Unsupported before launch (tagg.h TAGG_ERR_UNSUPPORTED), never a wrong
-    result."""
+    """K is bounded by the S_B staging (128 k-blocks): every K <= 16384 runs -- the S_A window
+    drops to one slot when two do not fit beside two pipeline stages -- and K = 16512 raises
+    Unsupported before launch (tagg.h TAGG_ERR_UNSUPPORTED), never a wrong result."""
     sizes = (130, 1, 256)
     n = 128
-    for k in (15872, 16128, 16256):
+    for k in (15872, 16384, 16512):
         ac, asc, bc, bsc = _synthetic(sizes, n, k, k)
         args = (_dev(ac), _dev(asc), _dev(bc), _dev(bsc), _dev(np.array(sizes, np.int32)))
-        if k == 16256:
+        if k == 16512:
             with pytest.raises(tg.Unsupported):
                 tg.grouped_gemm_fp8(*args)
             continue

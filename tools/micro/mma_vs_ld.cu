@@ -291,5 +291,7 @@ int main() {
   run<0, 2, 1, 64>("cg2: no drain, A MN-major, B MN-major");
   run<1, 2, 1, 0>("cg2: 32x32b.x32 drain, A K, B MN");
   run<1, 2, 1, 64>("cg2: 32x32b.x32 drain, A MN, B MN");
+  run<0, 2, 1, 0>("cg2: no drain, A K, B MN", 1);
+  run<1, 2, 1, 0>("cg2: 32x32b.x32 drain, A K, B MN", 1);
   return 0;
 }

@@ -16,7 +16,6 @@ using namespace tagg;
 
 constexpr int kPromo = 8;
 constexpr int kThreads = 32 * (4 + kPromo);
-constexpr int NS = 4;  // stages
 constexpr int KB = 64;  // k-blocks per tile (K = 8192)
 
 struct P {
@@ -24,10 +23,12 @@ struct P {
 };
 
 // MODE 0: no drain.  1: drain + FFMA2 (late release).  2: drain + FFMA2 (early release)
+// 3: the kernel's drain (two 32x32b.x64 loads, release after the second, math between)
 // LOAD 0: producer only arrives (no TMA).  1: TMA A + B.
 // X bit 0: scale s from two ld.shared one k-block ahead; bit 1: epilogue (bf16 -> smem
-// staging -> TMA store) every KB k-blocks; bit 2: MMA waits full before tempty
-template <int MODE, int LOAD, int X = 0>
+// staging -> TMA store) every KB k-blocks; bit 2: MMA waits full before tempty;
+// bit 4: pair cid reads B n-tile cid % 16 of a [K, 4096] B (distinct B per pair)
+template <int MODE, int LOAD, int X = 0, int NS = 4>
 __global__ void __launch_bounds__(kThreads, 1) gemm(const __grid_constant__ P p, int reps, unsigned long long* out,
                                                     float* sink) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm(const __grid_constant__ P p,
           if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (16384 + 16384));
           const int kb = i % KB;
           tma_load_2d_cg2(&p.ta, &full[s], sA + s * 16384, kb * 128, cid * 256 + rank * 128);
-          tma_load_3d_cg2(&p.tb, &full[s], sB + s * 16384, rank * 128, kb * 128, 0);
+          tma_load_3d_cg2(&p.tb, &full[s], sB + s * 16384, ((X & 16) ? (cid % 16) * 256 : 0) + rank * 128, kb * 128, 0);
         } else if (rank == 0) {
           mbar_arrive(&full[s]);
         }
@@ -121,7 +122,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm(const __grid_constant__ P p,
       }
       mbar_wait(&tfull[b], (i >> 1) & 1);
       tc_fence_after();
-      if (MODE != 0) {
+      if (MODE == 3) {
+        const uint32_t ta = ta0 + b * 256;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[64];
+          tmem_ld_32x32b_x64(ta + 64 * c, v);
+          tmem_wait_ld_dep64(v);
+          if (c == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader(&tempty[b]);
+          }
+#pragma unroll
+          for (int j = 0; j < 64; j += 2)
+            ffma2(acc[64 * c + j], acc[64 * c + j + 1], __uint_as_float(v[j]), __uint_as_float(v[j + 1]), s);
+        }
+      } else if (MODE != 0) {
         const uint32_t ta = ta0 + b * 256;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -138,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm(const __grid_constant__ P p,
             ffma2(acc[32 * c + j], acc[32 * c + j + 1], __uint_as_float(v[j]), __uint_as_float(v[j + 1]), s);
         }
       }
-      if (MODE != 2) {
+      if (MODE != 2 && MODE != 3) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_leader(&tempty[b]);
@@ -196,11 +213,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 enc() {
   return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
 }
 
-template <int MODE, int LOAD, int X = 0>
+template <int MODE, int LOAD, int X = 0, int NS = 4>
 void run(const char* name, const P& p, unsigned long long* d_out, float* sink) {
   const int reps = 32;
   const int smem = 2 * NS * 16384 + 32768 + 1024;
-  cudaFuncSetAttribute(gemm<MODE, LOAD, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gemm<MODE, LOAD, X, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148);
   cfg.blockDim = dim3(kThreads);
@@ -212,12 +229,12 @@ void run(const char* name, const P& p, unsigned long long* d_out, float* sink) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm<MODE, LOAD, X>, p, reps, d_out, sink);
+  cudaLaunchKernelEx(&cfg, gemm<MODE, LOAD, X, NS>, p, reps, d_out, sink);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int it = 0; it < 5; ++it) cudaLaunchKernelEx(&cfg, gemm<MODE, LOAD, X>, p, reps, d_out, sink);
+  for (int it = 0; it < 5; ++it) cudaLaunchKernelEx(&cfg, gemm<MODE, LOAD, X, NS>, p, reps, d_out, sink);
   cudaEventRecord(e1);
   const cudaError_t e = cudaDeviceSynchronize();
   float ms = 0;
@@ -232,7 +249,7 @@ void run(const char* name, const P& p, unsigned long long* d_out, float* sink) {
 }
 
 int main() {
-  const int M = 256 * 74, K = 8192, N = 256;
+  const int M = 256 * 74, K = 8192, N = 4096;
   uint8_t *a, *b;
   cudaMalloc(&a, size_t(M) * K);
   cudaMalloc(&b, size_t(K) * N);
@@ -243,7 +260,7 @@ int main() {
     v = static_cast<uint8_t>(x >> 24) & 0xFE;
   }
   cudaMemcpy(a, h.data(), size_t(M) * K, cudaMemcpyHostToDevice);
-  cudaMemcpy(b, h.data(), size_t(K) * N, cudaMemcpyHostToDevice);
+  cudaMemcpy(b, h.data(), size_t(K) * N, cudaMemcpyHostToDevice);  // K*N <= M*K
   P p;
   auto fn = enc();
   {
@@ -270,10 +287,14 @@ int main() {
   float* sink;
   cudaMalloc(&d_out, 148 * 8);
   cudaMalloc(&sink, 148 * kThreads * 4);
-  run<0, 0>("no TMA, no drain", p, d_out, sink);
   run<0, 1>("TMA, no drain", p, d_out, sink);
-  run<2, 0>("no TMA, drain (early release)", p, d_out, sink);
-  run<2, 1>("TMA, drain (early release)", p, d_out, sink);
-  run<2, 1, 2>("TMA, drain, + epilogue", p, d_out, sink);
+  run<2, 1>("TMA, drain x32 (early release)", p, d_out, sink);
+  run<3, 1>("TMA, drain x64 kernel-style", p, d_out, sink);
+  run<3, 1, 0, 3>("TMA, drain x64, 3 stages", p, d_out, sink);
+  run<3, 1, 1>("TMA, drain x64, s from smem", p, d_out, sink);
+  run<3, 1, 16>("TMA, drain x64, distinct B", p, d_out, sink);
+  run<3, 1, 2>("TMA, drain x64, epilogue", p, d_out, sink);
+  run<3, 1, 19, 3>("TMA, drain x64, all, 3 stages", p, d_out, sink);
+  run<2, 1, 19, 3>("TMA, drain x32, all, 3 stages", p, d_out, sink);
   return 0;
 }
