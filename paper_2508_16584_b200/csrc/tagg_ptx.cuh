@@ -475,6 +475,19 @@ __device__ __forceinline__ void fmul2s(float& d0, float& d1, float a0, float a1,
       : "f"(a0), "f"(a1), "f"(s));
 }
 
+// (d0, d1) = RZ((a0, a1) * (b0, b1)): one packed FMUL2 rounding toward zero.
+__device__ __forceinline__ void fmul2_rz(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n"
+      ".reg .b64 pa, pb, pd;\n"
+      "mov.b64 pa, {%2, %3};\n"
+      "mov.b64 pb, {%4, %5};\n"
+      "mul.rz.f32x2 pd, pa, pb;\n"
+      "mov.b64 {%0, %1}, pd;\n"
+      "}\n"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 // The reference's two roundings on a pair, acc = fl(acc + fl(p * s)) (engine.py:161-164), in two
 // packed instructions: t = FMUL2(p, s), then acc = FFMA2(t, one, acc) = fl(acc + t) exactly
 // (t * 1 is exact).  `one` must be opaque to ptxas (a value it cannot prove is 1.0): it then

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "tagg.h"
 #include "tagg_host.h"
@@ -431,25 +432,103 @@ __global__ void __launch_bounds__(128) quantize_col_blocks_kernel(const void* __
   if (bad) atomicOr(err, 2);
 }
 
-// Vector form: thread = 8 consecutive columns (16-B bf16 / 32-B f32 loads, 8-B code stores),
-// 64 threads = 512 columns per CTA; the (group, token block) lookup is the same table walk.
+// e4m3 codes of four quotients x / s (fp8.py:54-80: fp32 x / s, then round to e4m3).  The
+// exact fp32 quotient lies between RZ(x * RD(1/s)) and RZ(x * r_hi) with r_hi >= (1/s)(1 + 2^-22)
+// (both bounds toward zero, so the bracket holds for either sign); fp32 rounding and the e4m3
+// conversion (rn, satfinite) are monotonic, so when both bounds give the same codes those ARE
+// the codes of RN(x / s).  Otherwise -- a bound pair straddling an e4m3 rounding midpoint, a few
+// in a million -- the IEEE division decides.  Two multiplies and a conversion per element
+// instead of the ~10-instruction __fdiv_rn.
+__device__ __forceinline__ uint32_t e4m3x4_bracket(const float (&v)[4], const float (&rlo)[4],
+                                                   const float (&rhi)[4], uint32_t& hi_codes) {
+  float l[4], u[4];  // packed FMUL2.RZ: one instruction per pair
+  fmul2_rz(l[0], l[1], v[0], v[1], rlo[0], rlo[1]);
+  fmul2_rz(l[2], l[3], v[2], v[3], rlo[2], rlo[3]);
+  fmul2_rz(u[0], u[1], v[0], v[1], rhi[0], rhi[1]);
+  fmul2_rz(u[2], u[3], v[2], v[3], rhi[2], rhi[3]);
+  uint16_t a, b, c, d;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(a) : "f"(l[1]), "f"(l[0]));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(b) : "f"(l[3]), "f"(l[2]));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(c) : "f"(u[1]), "f"(u[0]));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(d) : "f"(u[3]), "f"(u[2]));
+  hi_codes = static_cast<uint32_t>(c) | (static_cast<uint32_t>(d) << 16);
+  return static_cast<uint32_t>(a) | (static_cast<uint32_t>(b) << 16);
+}
+// The bracket's undecided case (a few per thousand elements: bf16 data over a bf16 column
+// maximum puts x / s on or next to an e4m3 midpoint that often): the IEEE division decides.
+__device__ __forceinline__ uint32_t e4m3x4_div(const float4 v, const float* s) {
+  uint16_t a, b;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(a) : "f"(__fdiv_rn(v.y, s[1])), "f"(__fdiv_rn(v.x, s[0])));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(b) : "f"(__fdiv_rn(v.w, s[3])), "f"(__fdiv_rn(v.z, s[2])));
+  return static_cast<uint32_t>(a) | (static_cast<uint32_t>(b) << 16);
+}
+
+// Column-block quantizer, register tiles: CTA = one (group, 128-token block); it walks the
+// group table once, then sweeps the columns 128 at a time.  Thread t holds columns
+// [8 (t % 16), +8) of rows t / 16 + 16 j, j < 8, in registers, so x is read ONCE from HBM (a
+// two-pass form re-read it, and the re-read missed L2); bf16 chunks are prefetched one ahead.
+// Column maxima: integer max of |x| bit patterns (packed bf16 pairs: one VIMNMX per two
+// elements; NaN > inf > finite, so the same max flags non-finite input), a shuffle between the
+// two row lanes of a warp, then the 8 warps via smem.
 // kBlock128: one scale per (token block, 128 columns) -- the reference's 128x128 block recipe
 // (fp8.py:154-176) applied to each group's token blocks -- written to all 128 columns' scale
 // slots, so the wgrad can promote with one scale per drained 128-column half (1 op per pair).
-template <bool kBf16, bool kBlock128 = false>
-// Optional gather: grouped row r reads row_weights[r] * x[index[r]] (index / row_weights
-// nullable), so token-ordered activations are quantized into the grouped layout without a copy.
-__global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* __restrict__ x, int64_t ldx, int cols,
-                                                                    const int32_t* __restrict__ group_sizes, int G,
-                                                                    uint8_t* __restrict__ codes, int64_t ldc,
-                                                                    float* __restrict__ scales, int32_t* err,
-                                                                    const int32_t* __restrict__ index,
-                                                                    const float* __restrict__ row_weights) {
+// kWeighted / index: grouped row r reads row_weights[r] * x[index[r]] (index nullable), so
+// token-ordered activations are quantized into the grouped layout without a copy.
+template <bool kBf16>
+struct ColChunk {
+  using Raw = typename std::conditional<kBf16, uint4, float4[2]>::type;
+  Raw raw[8];
+  __device__ __forceinline__ void load(const void* x, int64_t ldx, const int64_t (&src)[8], int c) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if constexpr (kBf16) {
+        raw[j] = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + src[j] * ldx + c));
+      } else {
+        const float4* f = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + src[j] * ldx + c);
+        raw[j][0] = __ldcs(f);
+        raw[j][1] = __ldcs(f + 1);
+      }
+    }
+  }
+  __device__ __forceinline__ uint32_t word(int j, int h) const {  // bf16 pair h of row j
+    if constexpr (kBf16) return h == 0 ? raw[j].x : h == 1 ? raw[j].y : h == 2 ? raw[j].z : raw[j].w;
+    else return 0u;
+  }
+  __device__ __forceinline__ float get(int j, int k) const {
+    if constexpr (kBf16) {
+      const uint32_t w = word(j, k >> 1);
+      return __uint_as_float((k & 1) ? (w & 0xFFFF0000u) : (w << 16));
+    } else {
+      const float4& q = raw[j][k >> 2];
+      return (k & 3) == 0 ? q.x : (k & 3) == 1 ? q.y : (k & 3) == 2 ? q.z : q.w;
+    }
+  }
+};
+
+template <bool kBf16, bool kBlock128, bool kWeighted>
+__global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* __restrict__ x, int64_t ldx, int cols,
+                                                                   const int32_t* __restrict__ group_sizes, int G,
+                                                                   uint8_t* __restrict__ codes, int64_t ldc,
+                                                                   float* __restrict__ scales, int32_t* err,
+                                                                   const int32_t* __restrict__ index,
+                                                                   const float* __restrict__ row_weights) {
   __shared__ int32_t s_row0, s_rows, s_tb;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
+  __shared__ __align__(16) uint32_t s_part[2][8][128];  // per-warp column maxima (|x| bits)
+  __shared__ __align__(16) float s_scale[2][128];
+  __shared__ __align__(16) float s_rlo[2][128];
+  __shared__ __align__(16) float s_rhi[2][128];
+  // per-warp queue of undecided 4-column groups (values, row, column): a warp resolves them 32
+  // at a time, one group per lane, instead of every lane idling through one lane's divisions
+  constexpr int kQueue = 64;
+  __shared__ __align__(16) float4 q_v[8][kQueue][2];
+  __shared__ int32_t q_r[8][kQueue];
+  __shared__ uint32_t s_bmax[2][4];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t < 32) {
+    // which (group, block) is this CTA's: walk the group table
     int carry_r = 0, carry_b = 0, found = 0;
-    const int want = blockIdx.y;
+    const int want = blockIdx.x;
     for (int base = 0; base < G && !found; base += 32) {
       const int g = base + lane;
       const int m = (g < G) ? max(0, group_sizes[g]) : 0;
@@ -481,76 +560,153 @@ __global__ void __launch_bounds__(64) quantize_col_blocks_v8_kernel(const void* 
   const int rows = s_rows;
   if (rows <= 0) return;
   const int64_t row0 = s_row0;
-  const int c0 = (blockIdx.x * 64 + threadIdx.x) * 8;
-  // kBlock128: cols % 128 == 0, so the 16 lanes of a 128-column block are all in or all out
-  if (c0 >= cols) return;  // cols % 8 == 0 on this path
-  auto load8 = [&](int64_t r_grouped, float (&v)[8]) {
-    const int64_t rr = index ? static_cast<int64_t>(index[r_grouped]) : r_grouped;
-    const float wr = row_weights ? row_weights[r_grouped] : 1.0f;
-    if constexpr (kBf16) {
-      const uint4 q = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + rr * ldx + c0);
-      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  const int64_t tb = s_tb;
+  const int cg = t & 15, rl = t >> 4;
+  // Rows past the block read a clamped live row: all 8 loads go out without a branch, and a
+  // duplicate of a live row leaves every column maximum unchanged (such rows are never stored).
+  // Columns past `cols` read a clamped live column the same way (their scales are not written).
+  int64_t src[8];
+  float wr[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        v[2 * j] = __uint_as_float(w[j] << 16);
-        v[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+  for (int j = 0; j < 8; ++j) {
+    const int64_t rg = row0 + min(rl + 16 * j, rows - 1);
+    src[j] = index ? static_cast<int64_t>(__ldg(index + rg)) : rg;
+    wr[j] = kWeighted ? __ldg(row_weights + rg) : 1.0f;
+  }
+  auto value = [&](const ColChunk<kBf16>& ch, int j, int k) -> float {
+    const float f = ch.get(j, k);
+    return kWeighted ? __fmul_rn(wr[j], f) : f;  // weighted rows are fl(w * x), as gathered
+  };
+  const int nchunks = (cols + 127) / 128;  // cols % 8 == 0 on this path (kBlock128: % 128)
+  uint32_t bad = 0;
+  // bf16: the next chunk's loads are in flight while this one is reduced and quantized (two
+  // 32-register chunks); f32 chunks take 64 registers each, so f32 loads one at a time
+  // (measured: without the prefetch, 3 CTAs per SM run 3-5% slower)
+  constexpr bool kPrefetch = kBf16;
+  ColChunk<kBf16> cur;
+  if (kPrefetch) cur.load(x, ldx, src, min(cg * 8, cols - 8));
+  for (int cb = 0; cb < nchunks; ++cb) {
+    const int c0 = cb * 128 + cg * 8;
+    ColChunk<kBf16> nxt;
+    if (!kPrefetch) cur.load(x, ldx, src, min(c0, cols - 8));
+    if (kPrefetch && cb + 1 < nchunks) nxt.load(x, ldx, src, min(c0 + 128, cols - 8));
+    const int buf = cb & 1;
+    uint32_t amax[8];  // |x| bit patterns: integer order = float order for non-negative floats
+    if constexpr (kBf16 && !kWeighted) {
+      uint32_t pw[4] = {0u, 0u, 0u, 0u};  // packed pairs
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) pw[h] = __vmaxu2(pw[h], cur.word(j, h) & 0x7FFF7FFFu);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        amax[2 * h] = pw[h] << 16;
+        amax[2 * h + 1] = pw[h] & 0xFFFF0000u;
       }
     } else {
-      const float4* f = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + rr * ldx + c0);
-      const float4 a = f[0], b = f[1];
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) amax[k] = 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) amax[k] = max(amax[k], __float_as_uint(value(cur, j, k)) & 0x7FFFFFFFu);
     }
-    if (row_weights) {
+    // the two row lanes of this warp that share the columns, then the 8 warps
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __fmul_rn(wr, v[j]);
+    for (int k = 0; k < 8; ++k) amax[k] = max(amax[k], __shfl_xor_sync(0xffffffffu, amax[k], 16));
+    if (lane < 16) {
+      uint4* dst = reinterpret_cast<uint4*>(&s_part[buf][warp][cg * 8]);
+      dst[0] = make_uint4(amax[0], amax[1], amax[2], amax[3]);
+      dst[1] = make_uint4(amax[4], amax[5], amax[6], amax[7]);
     }
-  };
-  float amax[8];
+    __syncthreads();
+    uint32_t cm = 0u;
+    if (t < 128) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) amax[j] = 0.0f;
-  bool bad = false;
-#pragma unroll 4
-  for (int i = 0; i < rows; ++i) {
-    float v[8];
-    load8(row0 + i, v);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float m = fabsf(v[j]);
-      bad |= !(m <= 3.402823466e38f);
-      amax[j] = fmaxf(amax[j], m);
+      for (int w = 0; w < 8; ++w) cm = max(cm, s_part[buf][w][t]);
+      if (cb * 128 + t < cols) bad |= cm >= 0x7F800000u;  // inf or NaN in a live column
     }
-  }
-  if constexpr (kBlock128) {
-    float bm = amax[0];
+    if constexpr (kBlock128) {
+      // one scale per 128-column block: the max over the block's columns (warps 0-3)
 #pragma unroll
-    for (int j = 1; j < 8; ++j) bm = fmaxf(bm, amax[j]);
-    const unsigned half_mask = 0xFFFFu << (threadIdx.x & 16);  // this 128-column block's 16 lanes
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(half_mask, bm, o));
-#pragma unroll
-    for (int j = 0; j < 8; ++j) amax[j] = bm;
-  }
-  float s[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) s[j] = amax[j] > 0.0f ? __fdiv_rn(amax[j], 448.0f) : 1.0f;
-  float4* sdst = reinterpret_cast<float4*>(scales + static_cast<int64_t>(s_tb) * cols + c0);
-  sdst[0] = make_float4(s[0], s[1], s[2], s[3]);
-  sdst[1] = make_float4(s[4], s[5], s[6], s[7]);
-#pragma unroll 4
-  for (int i = 0; i < rows; ++i) {
-    float v[8];
-    load8(row0 + i, v);
-    uint32_t w[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      uint16_t lo, hi;
-      const float a0 = __fdiv_rn(v[4 * h], s[4 * h]), a1 = __fdiv_rn(v[4 * h + 1], s[4 * h + 1]);
-      const float a2 = __fdiv_rn(v[4 * h + 2], s[4 * h + 2]), a3 = __fdiv_rn(v[4 * h + 3], s[4 * h + 3]);
-      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(a1), "f"(a0));
-      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(a3), "f"(a2));
-      w[h] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+      for (int o = 16; o > 0; o >>= 1) cm = max(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+      if (t < 128 && lane == 0) s_bmax[buf][warp] = cm;
+      __syncthreads();
+      cm = max(max(s_bmax[buf][0], s_bmax[buf][1]), max(s_bmax[buf][2], s_bmax[buf][3]));
     }
-    *reinterpret_cast<uint2*>(codes + (row0 + i) * ldc + c0) = make_uint2(w[0], w[1]);
+    if (t < 128) {
+      const float am = __uint_as_float(cm);
+      const float sc = am > 0.0f ? __fdiv_rn(am, 448.0f) : 1.0f;
+      const float rd = __frcp_rd(sc);
+      s_scale[buf][t] = sc;
+      s_rlo[buf][t] = rd;
+      // >= (1/s)(1 + 2^-22): RU(1/s) raised by two ulps (or 1/s overflowing to inf)
+      const float ru = __frcp_ru(sc);
+      s_rhi[buf][t] = isinf(ru) ? ru : __uint_as_float(__float_as_uint(ru) + 2u);
+      const int c = cb * 128 + t;
+      if (c < cols) scales[tb * cols + c] = sc;
+    }
+    __syncthreads();
+    {
+      const bool c_ok = c0 < cols;
+      float rlo[8], rhi[8];
+      {
+        const float4* pl = reinterpret_cast<const float4*>(&s_rlo[buf][cg * 8]);
+        const float4* ph = reinterpret_cast<const float4*>(&s_rhi[buf][cg * 8]);
+        const float4 a = pl[0], b = pl[1], e = ph[0], f = ph[1];
+        rlo[0] = a.x; rlo[1] = a.y; rlo[2] = a.z; rlo[3] = a.w; rlo[4] = b.x; rlo[5] = b.y; rlo[6] = b.z; rlo[7] = b.w;
+        rhi[0] = e.x; rhi[1] = e.y; rhi[2] = e.z; rhi[3] = e.w; rhi[4] = f.x; rhi[5] = f.y; rhi[6] = f.z; rhi[7] = f.w;
+      }
+      const uint32_t lt = (1u << lane) - 1u;
+      uint8_t* const crow = codes + (row0 + rl) * ldc + c0;  // this thread's first row
+      int qn = 0;  // warp-uniform
+      auto drain_queue = [&]() {
+        __syncwarp();  // the rows' bracket codes are stored before any patch
+        for (int base = 0; base < qn; base += 32) {
+          const int i = base + lane;
+          if (i < qn) {
+            const int rc = q_r[warp][i];  // row << 8 | 8-column group
+            const int cc = cb * 128 + (rc & 0xFF) * 8;
+            const uint32_t w0 = e4m3x4_div(q_v[warp][i][0], &s_scale[buf][cc - cb * 128]);
+            const uint32_t w1 = e4m3x4_div(q_v[warp][i][1], &s_scale[buf][cc - cb * 128 + 4]);
+            *reinterpret_cast<uint2*>(codes + (row0 + (rc >> 8)) * ldc + cc) = make_uint2(w0, w1);
+          }
+        }
+        __syncwarp();
+        qn = 0;
+      };
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = rl + 16 * j;
+        const bool live = c_ok && r < rows;
+        uint32_t w[2], up[2];
+        float4 vv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float v4[4] = {value(cur, j, 4 * h), value(cur, j, 4 * h + 1), value(cur, j, 4 * h + 2),
+                               value(cur, j, 4 * h + 3)};
+          const float l4[4] = {rlo[4 * h], rlo[4 * h + 1], rlo[4 * h + 2], rlo[4 * h + 3]};
+          const float h4[4] = {rhi[4 * h], rhi[4 * h + 1], rhi[4 * h + 2], rhi[4 * h + 3]};
+          w[h] = e4m3x4_bracket(v4, l4, h4, up[h]);
+          vv[h] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+        }
+        if (live) *reinterpret_cast<uint2*>(crow + static_cast<int64_t>(16 * j) * ldc) = make_uint2(w[0], w[1]);
+        const bool u = live && (w[0] != up[0] || w[1] != up[1]);
+        const uint32_t m = __ballot_sync(0xffffffffu, u);
+        if (m) {
+          if (u) {
+            const int pos = qn + __popc(m & lt);
+            q_v[warp][pos][0] = vv[0];
+            q_v[warp][pos][1] = vv[1];
+            q_r[warp][pos] = (r << 8) | cg;
+          }
+          qn += __popc(m);
+        }
+        if (qn >= 32) drain_queue();  // < 32 + 32 entries: fits kQueue
+      }
+      if (qn) drain_queue();
+    }
+    if (kPrefetch) cur = nxt;
   }
   if (bad) atomicOr(err, 2);
 }
@@ -618,26 +774,21 @@ static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc,
   const int esz = x_dtype == TAGG_DTYPE_BF16 ? 2 : 4;
   const bool v8 = cols % 8 == 0 && !(reinterpret_cast<uintptr_t>(x) % 16) && !((ldx * esz) % 16) &&
                   !(reinterpret_cast<uintptr_t>(codes) % 8) && !(ldc % 8) && !(reinterpret_cast<uintptr_t>(scales) % 16);
-  if (v8 && block_cols == 128) {
-    const dim3 g8(static_cast<unsigned>((cols / 8 + 63) / 64), static_cast<unsigned>(tb));
-    if (x_dtype == TAGG_DTYPE_BF16)
-      wg::quantize_col_blocks_v8_kernel<true, true><<<g8, 64, 0, st>>>(
-          x, ldx, cols, group_sizes, G, static_cast<uint8_t*>(codes), ldc, scales, err_flag, index, row_weights);
-    else
-      wg::quantize_col_blocks_v8_kernel<false, true><<<g8, 64, 0, st>>>(
-          x, ldx, cols, group_sizes, G, static_cast<uint8_t*>(codes), ldc, scales, err_flag, index, row_weights);
-    return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
-  }
   if (v8) {
-    const dim3 g8(static_cast<unsigned>((cols / 8 + 63) / 64), static_cast<unsigned>(tb));
-    if (x_dtype == TAGG_DTYPE_BF16)
-      wg::quantize_col_blocks_v8_kernel<true><<<g8, 64, 0, st>>>(x, ldx, cols, group_sizes, G,
-                                                                 static_cast<uint8_t*>(codes), ldc, scales, err_flag,
-                                                                 index, row_weights);
-    else
-      wg::quantize_col_blocks_v8_kernel<false><<<g8, 64, 0, st>>>(x, ldx, cols, group_sizes, G,
-                                                                  static_cast<uint8_t*>(codes), ldc, scales, err_flag,
-                                                                  index, row_weights);
+    const dim3 gt(static_cast<unsigned>(tb));
+    auto launch = [&](auto kern) {
+      kern<<<gt, 256, 0, st>>>(x, ldx, cols, group_sizes, G, static_cast<uint8_t*>(codes), ldc, scales, err_flag, index,
+                               row_weights);
+    };
+    const bool bf16 = x_dtype == TAGG_DTYPE_BF16, w = row_weights != nullptr, b128 = block_cols == 128;
+    using namespace wg;
+    if (bf16) {
+      if (b128) w ? launch(quantize_col_tile_kernel<true, true, true>) : launch(quantize_col_tile_kernel<true, true, false>);
+      else w ? launch(quantize_col_tile_kernel<true, false, true>) : launch(quantize_col_tile_kernel<true, false, false>);
+    } else {
+      if (b128) w ? launch(quantize_col_tile_kernel<false, true, true>) : launch(quantize_col_tile_kernel<false, true, false>);
+      else w ? launch(quantize_col_tile_kernel<false, false, true>) : launch(quantize_col_tile_kernel<false, false, false>);
+    }
     return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
   }
   const dim3 grid(static_cast<unsigned>((cols + 127) / 128), static_cast<unsigned>(tb));

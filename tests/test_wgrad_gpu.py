@@ -42,6 +42,51 @@ def test_quantize_col_blocks_is_bit_exact(sizes, dtype):
     np.testing.assert_array_equal(scales[:tb].cpu().numpy().view(np.uint32), want_s.view(np.uint32))
 
 
+def _midpoint_inputs(seed):
+    """Rows fl(M * s_j) for every e4m3 rounding midpoint M (and 1-3 fp32 ulp either side), with
+    a planted column maximum A_j in the first row of each 128-row block, so s_j = fl(A_j / 448)
+    and the quotient x / s_j lands on (or next to) a midpoint."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    vals = np.unique(np.abs(ofp8.DECODE_TABLE[np.isfinite(ofp8.DECODE_TABLE)]).astype(np.float64))
+    mids = ((vals[:-1] + vals[1:]) / 2).astype(np.float32)
+    ms = [mids]
+    for d in (1, 2, 3):
+        up, dn = mids.copy(), mids.copy()
+        for _ in range(d):
+            up = np.nextafter(up, np.float32(np.inf))
+            dn = np.nextafter(dn, np.float32(0))
+        ms += [up, dn]
+    m_all = np.concatenate(ms)
+    m_all = m_all[rng.permutation(m_all.size)]
+    cols = 256
+    amax = np.exp2(rng.uniform(-12, 12, size=cols)).astype(np.float32)
+    s = (amax / np.float32(448.0)).astype(np.float32)
+    rows = []
+    for b0 in range(0, m_all.size, 127):
+        blk = m_all[b0:b0 + 127]
+        sign = np.where(rng.random((blk.size, cols)) < 0.5, np.float32(-1), np.float32(1))
+        rows.append(amax[None, :])
+        rows.append((blk[:, None] * s[None, :] * sign).astype(np.float32))
+    return np.concatenate(rows).astype(np.float32)
+
+
+@pytest.mark.parametrize("block_cols", [1, 128])
+def test_quantize_col_blocks_quotients_at_e4m3_midpoints(block_cols):
+    """The kernel decides each code from q = x * RN(1/s) and hands the quotients that sit near
+    an e4m3 rounding midpoint (or in the e4m3 subnormal range) to the IEEE division: inputs whose
+    x / s land on every midpoint and 1-3 ulp around it, bit-exact against the oracle's fp32
+    division (fp8.py:54-80)."""
+    x = _midpoint_inputs(5)
+    m = x.shape[0]
+    sizes = (128 * (m // 256), m - 128 * (m // 256))
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    codes, scales = tg.quantize_col_blocks(torch.from_numpy(x).to(DEV), gs, check=True, block_cols=block_cols)
+    torch.cuda.synchronize()
+    want_c, want_s = ofp8.quantize_col_blocks(x, sizes, block_cols=block_cols)
+    np.testing.assert_array_equal(codes.cpu().numpy(), want_c)
+    np.testing.assert_array_equal(scales[:want_s.shape[0]].cpu().numpy().view(np.uint32), want_s.view(np.uint32))
+
+
 @pytest.mark.parametrize("sizes,k,n", [
     ((128,), 128, 128),
     ((300, 0, 1, 77, 256), 256, 384),
