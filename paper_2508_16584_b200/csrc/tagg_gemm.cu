@@ -512,10 +512,14 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
                 ? idesc_half
                 : idesc;
         for (int kb = 0; kb < kbc; ++kb) {
-          mbar_wait_addr(tempty0 + 8 * acc, accph ^ 1);
-          if (lane == 0) trace_stamp(p.trace, kEvMmaTempty, kiter);
+          // Operands first, then the TMEM buffer: the stage is almost always complete long before
+          // the buffer (the 2-buffer promotion chain sets the pace), and a try_wait right after
+          // another wait costs ~90 clk even on a completed barrier (tools/micro/nbuf.cu: 703 -> 656
+          // clk per k-block), so the cheap wait goes where it overlaps the chain.
           mbar_wait_addr(full0 + 8 * stage, phase);
           if (lane == 0) trace_stamp(p.trace, kEvMmaFull, kiter);
+          mbar_wait_addr(tempty0 + 8 * acc, accph ^ 1);
+          if (lane == 0) trace_stamp(p.trace, kEvMmaTempty, kiter);
           tc_fence_after();
           const uint64_t ad = a_desc0 + ((stage * kStageBytesA) >> 4);
           const uint64_t bd = b_desc0 + ((stage * C::kStageBytesB) >> 4);

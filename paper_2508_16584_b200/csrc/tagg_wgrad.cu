@@ -220,10 +220,11 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
       for (int t = cid; t < tiles; t += nclusters) {
         const int m = tab_m[t / (p.KT * p.NT)];
         for (int j = 0; j * BT < m; ++j) {
-          mbar_wait_addr(smem_u32(&tempty[acc]), accph ^ 1);
-          if (lane == 0) wg_stamp(p.trace, kWgMmaTempty, miter);
+          // operands first, then the TMEM buffer (see tagg_gemm.cu's MMA issuer)
           mbar_wait_addr(smem_u32(&full[stage]), phase);
           if (lane == 0) wg_stamp(p.trace, kWgMmaFull, miter);
+          mbar_wait_addr(smem_u32(&tempty[acc]), accph ^ 1);
+          if (lane == 0) wg_stamp(p.trace, kWgMmaTempty, miter);
           tc_fence_after();
           const uint64_t ad = a0 + ((stage * kStageA) >> 4), bd = b0 + ((stage * kStageB) >> 4);
           if (elect_one()) {
