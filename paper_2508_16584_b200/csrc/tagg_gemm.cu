@@ -48,6 +48,10 @@
 #include "tagg_host.h"
 #include "tagg_ptx.cuh"
 
+#ifndef TAGG_DRAIN_MODE
+#define TAGG_DRAIN_MODE 1
+#endif
+
 namespace tagg {
 
 constexpr int BM = 128, BK = 128;
@@ -703,6 +707,63 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
           continue;
         }
         const uint32_t taddr = tmem_base + t_lane + acc_i * C::kBN + half * kCPT;
+#if TAGG_DRAIN_MODE == 1
+        // TMEM drain in 32-column chunks, two in flight: chunks 2j and 2j+1 land together, chunk
+        // 2j's math runs while chunk 2j+2 loads into its registers; the buffer is handed back
+        // once the last chunk has landed.
+        if (!(dbg & kDbgNoMath)) {
+          constexpr int n32 = kCPT / 32;
+          uint32_t va[32], vb[32];
+          tmem_ld_32x32b_x32(taddr, va);
+          tmem_ld_32x32b_x32(taddr + 32, vb);
+          tmem_wait_ld_dep2(va, vb);
+          if (n32 == 2) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (kCG == 1) mbar_arrive_addr(tempty_b); else mbar_arrive_leader_addr(tempty_b);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < n32; c += 2) {
+            const bool more = c + 2 < n32;
+            if constexpr (kExact) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2)
+                fma2_two_roundings(acc[32 * c + i], acc[32 * c + i + 1], __uint_as_float(va[i]), __uint_as_float(va[i + 1]),
+                                   s, one);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2)
+                ffma2(acc[32 * c + i], acc[32 * c + i + 1], __uint_as_float(va[i]), __uint_as_float(va[i + 1]), s);
+            }
+            if (more) tmem_ld_32x32b_x32(taddr + 32 * (c + 2), va);
+            if constexpr (kExact) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2)
+                fma2_two_roundings(acc[32 * c + 32 + i], acc[32 * c + 33 + i], __uint_as_float(vb[i]),
+                                   __uint_as_float(vb[i + 1]), s, one);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2)
+                ffma2(acc[32 * c + 32 + i], acc[32 * c + 33 + i], __uint_as_float(vb[i]), __uint_as_float(vb[i + 1]), s);
+            }
+            if (more) {
+              tmem_ld_32x32b_x32(taddr + 32 * (c + 3), vb);
+              tmem_wait_ld_dep2(va, vb);
+              if (c + 4 == n32) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                  if constexpr (kCG == 1) mbar_arrive_addr(tempty_b); else mbar_arrive_leader_addr(tempty_b);
+                }
+                if (tr_a) trace_stamp(p.trace, kEvPromoFreed, kiter);
+              }
+            }
+          }
+        } else
+#endif
+        {
         // TMEM drain, 64 columns at a time; the buffer is handed back as soon as the
         // last chunk has landed in registers.
         constexpr int kChunks = kCPT / 64;
@@ -731,6 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             for (int i = 0; i < 64; i += 2)
               ffma2(acc[64 * c + i], acc[64 * c + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]), s);
           }
+        }
         }
         if (tr_a) trace_stamp(p.trace, kEvPromoDone, kiter);
         ++kiter;
