@@ -684,12 +684,15 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       float acc[kCPT];
 #pragma unroll
       for (int i = 0; i < kCPT; ++i) acc[i] = 0.0f;
-      // s = fl(sa * sb) (engine.py:161-164), computed one k-block ahead
+      // s = fl(sa * sb) (engine.py:161-164), computed one k-block ahead.  The next k-block's
+      // scales are loaded before the accumulator wait but multiplied only after this k-block's
+      // math: the S_A loads are 8-way bank-conflicted (224-B rows at K = 7168), and an FMUL
+      // right behind the wait would hold the warp on them after the buffer is already full.
       float s_next = __fmul_rn(ld_shared_f32(sa_row), ld_shared_f32(sb_colp));
       for (int kb = 0; kb < kbc; ++kb) {
         const float s = s_next;
-        if (kb + 1 < kbc)
-          s_next = __fmul_rn(ld_shared_f32(sa_row + 4u * (kb + 1)), ld_shared_f32(sb_colp + 4u * (kb + 1)));
+        const uint32_t nkb = 4u * static_cast<uint32_t>(kb + 1 < kbc ? kb + 1 : kb);
+        float sa_nx = ld_shared_f32(sa_row + nkb), sb_nx = ld_shared_f32(sb_colp + nkb);
         mbar_wait_addr(tfull0 + 8 * acc_i, accph);
         if (tr_a) trace_stamp(p.trace, kEvPromoFull, kiter);
         if (tr_b) trace_stamp(p.trace, kEvPromo2Full, kiter);
@@ -797,6 +800,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         if (tr_a) trace_stamp(p.trace, kEvPromoDone, kiter);
         ++kiter;
         if (++acc_i == C::kNumAcc) { acc_i = 0; accph ^= 1; }
+        asm volatile("" : "+f"(sa_nx), "+f"(sb_nx));  // keeps the FMUL behind this k-block's math
+        s_next = __fmul_rn(sa_nx, sb_nx);
       }
       release_window(sempty0 + 8 * sab, lane);
       if (++sab == p.sa_slots) { sab = 0; saph ^= 1; }

@@ -35,8 +35,9 @@ def report(tr, lo, hi, label):
     d = lambda a, b, sh=0: (t[EV.index(a), lo:hi] - t[EV.index(b), lo - sh:hi - sh])  # noqa: E731
     rows = {
         "mma issue period": d("mma_issued", "mma_issued", 1),
-        "mma wait tempty (after prev issue)": d("mma_tempty", "mma_issued", 1),
-        "mma wait full": d("mma_full", "mma_tempty"),
+        "mma wait full (after prev issue)": d("mma_full", "mma_issued", 1),
+        "mma wait tempty (after full)": d("mma_tempty", "mma_full"),
+        "mma tempty seen->issued": d("mma_issued", "mma_tempty"),
         "mma issue->promo sees full": d("promo_full", "mma_issued"),
         "promo wait full (after prev done)": d("promo_full", "promo_done", 1),
         "promo full->freed (drain)": d("promo_freed", "promo_full"),
@@ -71,13 +72,25 @@ if len(sys.argv) > 1 and sys.argv[1] == "longk":
     cases = [("longk", [(256 * 74,)], 256, 8192, 1)]
 for name, sizes, n, k, G in cases:
     P = Problem(torch, name, sizes, n, k, G, dev, seed=1)
-    for label, flags in [("full", 0), ("noprom", 512), ("neither", 256 | 512)]:
+    modes = [("full", 0), ("noload", 256), ("nomath", 1024), ("noprom", 512), ("neither", 256 | 512)]
+    for label, flags in modes:
         L.tagg_debug_trace(None)
         run(P, flags, G)
         L.tagg_debug_trace(ctypes.c_void_p(buf.data_ptr()))
         buf.zero_()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
         run(P, flags, G)
+        ev1.record()
         torch.cuda.synchronize()
+        t0 = buf[0].cpu().numpy().astype(np.float64)
+        iss = t0[EV.index("mma_issued")]
+        nz = iss[iss > 0]
+        if len(nz) > 10:
+            # CTA 0's issue stamps span (n-1) periods: clk over the launch's wall time ~ the SM clock
+            span = nz[-1] - nz[0]
+            print(f"  [{label}] launch {ev0.elapsed_time(ev1) * 1e3:.0f} us; CTA0 issue span {span:.0f} clk over "
+                  f"{len(nz)} k-blocks -> >= {span / (ev0.elapsed_time(ev1) * 1e3):.0f} MHz")
         L.tagg_debug_trace(None)
         import os
         win = os.environ.get("TRACE_WINDOW")
