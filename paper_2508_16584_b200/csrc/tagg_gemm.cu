@@ -100,6 +100,7 @@ struct Params {
   uint32_t dbg;
   uint32_t pdl_overlap;  // TAGG_FLAG_PDL_OVERLAP: inputs are not written by the previous grid
   uint64_t l2_a, l2_b;   // L2 eviction policies of the A / B tile loads (0 = no hint)
+  uint64_t l2_c;         // L2 eviction policy of the C stores (0 = no hint)
   float one;             // 1.0f (kExact promotion: an FFMA2 by a 1.0 the compiler cannot see)
   uint32_t stage_tx;     // bytes landing per pipeline stage (both CTAs): A box rows x 128 + B box
 };
@@ -266,6 +267,16 @@ __device__ __forceinline__ void load_scale_window(const Params& p, const Tile& T
     mbar_arrive_expect_tx_addr(sfull0 + 8 * sab, bulk);
     if (bulk) bulk_load_1d_addr(sSA0 + sab * p.sa_buf_bytes, src, bulk, sfull0 + 8 * sab);
   }
+}
+
+// One C store from the pool (descriptors.py:95-106).  C is never read back by this kernel, so
+// by default its lines enter L2 as evict-first and leave the A / B tiles that later tiles re-read
+// in place (p.l2_c = 0: no hint).
+__device__ __forceinline__ void store_c(const Params& p, int lg, const void* src, int32_t col, int32_t row) {
+  if (p.l2_c)
+    tma_store_2d_hint(&p.tmap_c[lg], src, col, row, p.l2_c);
+  else
+    tma_store_2d(&p.tmap_c[lg], src, col, row);
 }
 
 // The persistent grid's cluster count, re-read from %nctaid per use: kept live across the
@@ -652,9 +663,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             const int col = T.n0 + 64 * ch;
             if (col >= p.N) break;
             const uint8_t* chunk = sC + ch * kHalfChunk;
-            tma_store_2d(&p.tmap_c[lg], chunk, col, T.crow0);
+            store_c(p, lg, chunk, col, T.crow0);
             if (T.valid != BM / 2)
-              tma_store_2d(&p.tmap_c[lg], chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
+              store_c(p, lg, chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
                            T.crow0 + T.valid - d);
           }
           bulk_commit();
@@ -847,9 +858,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             const int col = T.n0 + 64 * ch;
             if (col >= p.N) break;
             const uint8_t* chunk = sC + ch * kChunkBytesC;
-            tma_store_2d(&p.tmap_c[lg], chunk, col, T.crow0);  // phase a
+            store_c(p, lg, chunk, col, T.crow0);  // phase a
             if (T.valid != BM)                                   // phase b (both, even if they coincide)
-              tma_store_2d(&p.tmap_c[lg], chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
+              store_c(p, lg, chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
                            T.crow0 + T.valid - d);
           }
           bulk_commit();
@@ -901,12 +912,12 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             if (col >= p.N) break;
             const uint8_t* chunk = sC + ch * kChunkBytesC;
             // phase a: smem rows [0, d) -> rows [crow0, crow0 + d)
-            tma_store_2d(&p.tmap_c[lg], chunk, col, T.crow0);
+            store_c(p, lg, chunk, col, T.crow0);
             // phase b: smem rows [valid - d, valid) -> rows [crow0 + valid - d, crow0 + valid).
             // A full tile is one store (engine.py:318-322); a residual tile issues both
             // phases even when they coincide (descriptors.py:14-16).
             if (T.valid != BM)
-              tma_store_2d(&p.tmap_c[lg], chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
+              store_c(p, lg, chunk + static_cast<uint32_t>(T.valid - d) * 128u, col,
                            T.crow0 + T.valid - d);
           }
           bulk_commit();
@@ -1367,6 +1378,12 @@ extern "C" int tagg_grouped_gemm_fp8_ex(const void* a, int64_t lda, const float*
     const uint64_t pol[4] = {0, kL2EvictFirst, kL2EvictLast, kL2EvictNormal};
     p.l2_a = pol[hint & 3];
     p.l2_b = pol[(hint >> 2) & 3];
+    // C stores: evict-first unless TAGG_C_HINT says otherwise (0 none / 1 first / 2 last / 3 normal)
+    static const int chint = [] {
+      const char* e = std::getenv("TAGG_C_HINT");
+      return e ? std::atoi(e) : 1;
+    }();
+    p.l2_c = pol[chint & 3];
   }
   if (cg == 1) e = launch_cfg<1, 128>(p, smem_bytes, grid, st, exact, swz, pdl);
   else if (bn == 128) e = launch_cfg<2, 128>(p, smem_bytes, grid, st, exact, swz, pdl);

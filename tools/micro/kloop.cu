@@ -14,35 +14,36 @@ constexpr int kThreads = 384;
 constexpr int kS = 4;  // stages, each A 16 KB + B 16 KB (MN-major)
 // V bits: 1 = scales from smem (else constant), 2 = trace stamps off, 4 = release before math (x64),
 //         8 = MMA waits stage full, 16 = MMA warp tempty-first
-template <int V>
+template <int V, int CG = 2>
 __global__ void __launch_bounds__(kThreads, 1) kloop(int nk, unsigned long long* out, float* sink,
                                                    unsigned long long* tr, float one) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t kStB = CG == 2 ? 16384 : 32768;  // B per stage: this CTA's 128 columns, or all 256 (CG 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + kS * 16384;
   constexpr int kKb = 56;  // scale window depth (the DeepSeek-V3 gate+up tile); k-block kb reads column kb % 56
-  float* sSA = reinterpret_cast<float*>(smem + 2 * kS * 16384);  // [128 rows][56] (rb = 224 B)
+  float* sSA = reinterpret_cast<float*>(smem + kS * (16384 + kStB));  // [128 rows][56] (rb = 224 B)
   float* sSB = sSA + 128 * kKb;                                   // [2][56]
   __shared__ uint64_t full[kS], empty[kS], tfull[2], tempty[2];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int i = threadIdx.x; i < 2 * kS * 16384 / 4; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kS * (16384 + kStB) / 4; i += blockDim.x) {
     uint32_t v = (i + 1) * 2654435761u ^ (blockIdx.x * 97u);
     v ^= v >> 13; v *= 0x5bd1e995u; v ^= v >> 15;
     reinterpret_cast<uint32_t*>(smem)[i] = v & 0xFEFEFEFEu;
   }
   for (int i = threadIdx.x; i < 130 * kKb; i += blockDim.x) sSA[i] = 0.001f * (1 + (i & 7));
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 16); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8 * CG); }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<2>(&slot, 512);
+  if (warp == 1) tmem_alloc<CG>(&slot, 512);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
-  cluster_sync();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const bool trace = !(V & 2) && blockIdx.x == 0;
   if (warp < 4) {
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(kThreads, 1) kloop(int nk, unsigned long long*
       }
     } else if (warp == 1 && rank == 0) {
       const uint32_t tmem_base = ld_shared_u32(smem_u32(&slot));
-      const uint32_t idesc = idesc_e4m3_f32(256, 256, true);
+      const uint32_t idesc = idesc_e4m3_f32(128 * CG, 256, true);
       const uint64_t a_desc0 = umma_desc_sw128(smem_u32(sA), 16, 1024);
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(sB), 16384, 1024);
       const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
@@ -71,15 +72,15 @@ __global__ void __launch_bounds__(kThreads, 1) kloop(int nk, unsigned long long*
         tc_fence_after();
         if (trace && lane == 0 && kb < 1024) tr[0 * 1024 + kb] = clock64();
         const uint64_t ad = a_desc0 + ((stage * 16384u) >> 4);
-        const uint64_t bd = b_desc0 + ((stage * 16384u) >> 4);
+        const uint64_t bd = b_desc0 + ((stage * kStB) >> 4);
         const uint32_t d_tmem = tmem_base + acc * 256;
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_f8f6f4<2>(d_tmem, ad + static_cast<uint64_t>(k * 2), bd + static_cast<uint64_t>(k * 256), idesc,
-                          k > 0 ? 1u : 0u);
-          mma_commit_addr<2>(empty0 + 8 * stage);
-          mma_commit_addr<2>(tfull0 + 8 * acc);
+            mma_f8f6f4<CG>(d_tmem, ad + static_cast<uint64_t>(k * 2), bd + static_cast<uint64_t>(k * 256), idesc,
+                           k > 0 ? 1u : 0u);
+          mma_commit_addr<CG>(empty0 + 8 * stage);
+          mma_commit_addr<CG>(tfull0 + 8 * acc);
         }
         __syncwarp();
         if (trace && lane == 0 && kb < 1024) tr[1 * 1024 + kb] = clock64();
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1) kloop(int nk, unsigned long long*
           if (c == 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_leader_addr(tempty_b);
+            if (lane == 0) { if (CG == 2) mbar_arrive_leader_addr(tempty_b); else mbar_arrive_addr(tempty_b); }
             if (tr_a && kb < 1024) tr[3 * 1024 + kb] = clock64();
           }
 #pragma unroll
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) kloop(int nk, unsigned long long*
             tmem_wait_ld_dep2(va, vb);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_leader_addr(tempty_b);
+            if (lane == 0) { if (CG == 2) mbar_arrive_leader_addr(tempty_b); else mbar_arrive_addr(tempty_b); }
             if (tr_a && kb < 1024) tr[3 * 1024 + kb] = clock64();
           }
         }
@@ -166,10 +167,10 @@ __global__ void __launch_bounds__(kThreads, 1) kloop(int nk, unsigned long long*
   }
   __syncthreads();
   tc_fence_before();
-  cluster_sync();
+  if (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<2>(ld_shared_u32(smem_u32(&slot)), 512);
+    tmem_dealloc<CG>(ld_shared_u32(smem_u32(&slot)), 512);
   }
 }
 
@@ -177,18 +178,18 @@ static unsigned long long* g_out;
 static float* g_sink;
 static unsigned long long* g_tr;
 
-template <int V>
+template <int V, int CG = 2>
 void run(const char* name) {
   const int nk = 56;  // the DeepSeek-V3 gate+up tile depth; launched as many "tiles" back to back
-  const int smem = 2 * kS * 16384 + (130 * 56) * 4 + 2048;
-  cudaFuncSetAttribute(kloop<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = kS * (16384 + (CG == 2 ? 16384 : 32768)) + (130 * 56) * 4 + 2048;
+  cudaFuncSetAttribute(kloop<V, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1] = {};
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -201,7 +202,7 @@ void run(const char* name) {
   float best = 1e30f;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    cudaLaunchKernelEx(&cfg, kloop<V>, nk_run, g_out, g_sink, g_tr, 1.0f);
+    cudaLaunchKernelEx(&cfg, kloop<V, CG>, nk_run, g_out, g_sink, g_tr, 1.0f);
     cudaEventRecord(e1);
     const cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
@@ -218,7 +219,7 @@ void run(const char* name) {
     std::sort(v, v + n);
     return v[n / 2];
   };
-  const double flops = 148.0 * 128 * 256 * 128 * 2.0 * nk_run;
+  const double flops = 148.0 * 128 * 256 * 128 * 2.0 * nk_run;  // per SM: 128 rows x 256 columns either way
   printf("%-40s %7.1f TFLOP/s  period %5.0f clk | issue->issued %4.0f | issued->promo full %5.0f | drain %4.0f | "
          "freed->issue(i+2) %4.0f\n",
          name, flops / (best * 1e-3) / 1e12, med(0, 0, 1), med(1, 0, 0), med(2, 1, 0), med(3, 2, 0), med(0, 3, 2));
@@ -230,11 +231,9 @@ int main() {
   cudaMalloc(&g_tr, 4 * 1024 * 8);
   cudaMemset(g_tr, 0, 4 * 1024 * 8);
   for (int pass = 0; pass < 2; ++pass) {
-    run<1 | 8>("kernel-like (smem scales, stage wait)");
-    run<8>("constant scale");
-    run<1>("no stage wait");
-    run<1 | 8 | 4>("x64 drain (release after 2nd x64)");
-    run<1 | 8 | 16>("tempty before stage");
+    run<1 | 8, 2>("pair M=256 (kernel-like)");
+    run<1 | 8, 1>("1-CTA M=128 N=256");
+    run<8, 1>("1-CTA, constant scale");
   }
   return 0;
 }
