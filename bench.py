@@ -715,6 +715,8 @@ def summarize(line, fp8_peak):
         if isinstance(v, dict) and isinstance(v.get("dy_block128"), dict):
             out.append(f"wgrad dY 128x128 {f(v['dy_block128']['tflops'])} TF/s "
                        f"{f(100 * v['dy_block128']['fp8_peak_frac'], 1)}%")
+        if isinstance(v, dict) and isinstance(v.get("mxfp8"), dict):
+            out.append(f"wgrad MXFP8 {f(v['mxfp8']['tflops'])} TF/s {f(100 * v['mxfp8']['fp8_peak_frac'], 1)}%")
     q = ex.get("quantize_dispatch_dsv3")
     if isinstance(q, dict) and "gbs" in q:
         out.append(f"quant+dispatch {f(q['gbs'])} GB/s {f(100 * q['hbm_frac'])}%")
@@ -801,7 +803,9 @@ def run_wgrad(torch, tg, dev, fp8_peak, iters=5, warmup=2):
     """dW_g = X_g^T dY_g for the DeepSeek-V3 gate+up shapes (32 local
     experts, skewed M_g, K=7168, N=4096): the ragged rows are the reduction axis.  Two dY
     recipes: per-(token block, column) scales (two packed ops per element pair in the
-    promotion) and 128x128 block scales (one FFMA2 per pair, TAGG_WGRAD_DY_BLOCK128)."""
+    promotion) and 128x128 block scales (one FFMA2 per pair, TAGG_WGRAD_DY_BLOCK128); and the
+    MXFP8 recipe (per-(token block, column) power-of-two scales for X and dY, applied by the
+    tensor core as E8M0 block scales with no promotion, TAGG_WGRAD_MX)."""
     _, sizes = deepseek_gateup_sizes(seed=0)
     sizes = [int(s) for s in sizes]
     m, k, n = sum(sizes), 7168, 4096
@@ -814,15 +818,21 @@ def run_wgrad(torch, tg, dev, fp8_peak, iters=5, warmup=2):
     flops = 2.0 * m * k * n
     res = {"groups": len(sizes), "rows": m, "K": k, "N": n, "dw_bytes": len(sizes) * k * n * 2,
            "tile": "CTA pair 256x256, cta_group::2"}
-    for label, block in (("per_column_dy", False), ("dy_block128", True)):
-        dc, ds = tg.quantize_col_blocks(dy, gs, block_cols=128 if block else 1)
+    xm, _, xf = tg.quantize_col_blocks_mx(x, gs)
+    dm, _, dfac = tg.quantize_col_blocks_mx(dy, gs)
+    for label, block, mx in (("per_column_dy", False, False), ("dy_block128", True, False), ("mxfp8", False, True)):
+        if mx:
+            fn = lambda: tg.wgrad_fp8_mx(xm, xf, dm, dfac, gs, out=dw)  # noqa: E731
+        else:
+            dc, ds = tg.quantize_col_blocks(dy, gs, block_cols=128 if block else 1)
+            fn = lambda: tg.wgrad_fp8(xc, xs, dc, ds, gs, out=dw, dy_block128=block)  # noqa: E731
         for _ in range(warmup):
-            tg.wgrad_fp8(xc, xs, dc, ds, gs, out=dw, dy_block128=block)
+            fn()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for _ in range(iters):
-            tg.wgrad_fp8(xc, xs, dc, ds, gs, out=dw, dy_block128=block)
+            fn()
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / iters

@@ -238,11 +238,32 @@ int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, const float* 
    promotion then uses one scale per drained 128-column half: one FFMA2 per element pair instead of
    an FMUL2 and an FFMA2. */
 #define TAGG_WGRAD_DY_BLOCK128 1u
+#define TAGG_WGRAD_MX 2u /* internal: the tagg_wgrad_fp8_mx path (rejected by tagg_wgrad_fp8_ex) */
 int tagg_wgrad_fp8_ex(const void* x, const float* sx, const void* dy, const float* sdy, int64_t m_alloc,
                       const int32_t* group_sizes, int G, int K, int N, void* dw, uint32_t flags, void* stream);
+/* ---- MXFP8 weight gradient: power-of-two scales applied by the tensor core ----
+ * tagg_quantize_col_blocks_mx: the column-block quantizer (row gather as in _gather / _ex, index
+ * and row_weights nullable) with every scale rounded up to a power of two,
+ * s = 2^ceil(log2(fl(amax / 448))) (1.0 when zero), so x / s is exact; besides the fp32 scales it
+ * writes sf: per (token block, 128 columns) a 512-B block of E8M0 bytes in the tcgen05.cp source
+ * layout (byte 16 l + 4 c + j = the exponent byte of column 32 c + l's scale, j = 0..3),
+ * [tagg_token_blocks_bound(rows, G), cols / 128, 512] bytes.  cols % 128 == 0.
+ * tagg_wgrad_fp8_mx: dW_g = X_g^T dY_g from such operands (x_sf / dy_sf the sf blocks): the tensor
+ * core applies the factors as block scales (tcgen05.mma kind::mxf8f6f4.block_scale) and accumulates
+ * each tile's whole token range in TMEM, with no per-block promotion -- the same real sum as
+ * tagg_wgrad_fp8 over the same operands, rounded in fp32 by the tensor core instead of per block. */
+int tagg_quantize_col_blocks_mx(const void* x, int x_dtype, int64_t ldx, const int32_t* index, const float* row_weights,
+                                int64_t rows, int cols, const int32_t* group_sizes, int G, void* codes, int64_t ldc,
+                                float* scales, void* sf, int32_t* err_flag, void* stream);
+int tagg_wgrad_fp8_mx(const void* x, const void* x_sf, const void* dy, const void* dy_sf, int64_t m_alloc,
+                      const int32_t* group_sizes, int G, int K, int N, void* dw, void* stream);
 /* Column-block quantization with a row gather (index / row_weights nullable, as above) and a block
    width: block_cols = 1 is tagg_quantize_col_blocks(_gather); block_cols = 128 takes one amax per
    (token block, 128 columns) and writes it to all 128 columns' scale slots (cols % 128 == 0). */
+/* OR'ed into block_cols: every scale is rounded up to a power of two, s = 2^ceil(log2(fl(amax / 448)))
+   (1.0 when zero), so x / s is exact and s is one E8M0 byte -- the MXFP8 recipe that
+   TAGG_WGRAD_MX consumes. */
+#define TAGG_QCB_SCALE_POW2 0x10000
 int tagg_quantize_col_blocks_ex(const void* x, int x_dtype, int64_t ldx, const int32_t* index,
                                 const float* row_weights, int64_t rows, int cols, const int32_t* group_sizes, int G,
                                 void* codes, int64_t ldc, float* scales, int32_t* err_flag, int block_cols,

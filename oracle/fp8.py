@@ -100,7 +100,17 @@ def bf16_bits_to_f32(bits) -> np.ndarray:
     return u.view(np.float32)
 
 
-def quantize_col_blocks(x, group_sizes, block_cols: int = 1):
+def pow2_ceil(s):
+    """The smallest power of two >= s (fp32, s > 0; at least 2^-126): the UE8M0-representable
+    scale of the MXFP8 weight-gradient recipe (quantize_col_blocks(..., scale_pow2=True))."""
+    b = np.asarray(s, dtype=np.float32).view(np.uint32).copy()
+    up = (b & 0x7FFFFF) != 0
+    b = np.where(up, (b & 0xFF800000) + 0x800000, b).astype(np.uint32)
+    b = np.maximum(b, np.uint32(0x00800000))
+    return b.view(np.float32)
+
+
+def quantize_col_blocks(x, group_sizes, block_cols: int = 1, scale_pow2: bool = False):
     """Per-group 128x1 quantization for the weight gradient (the ragged token axis is the
     reduction axis): for each group and each of its 128-token blocks, one scale per
     column, s = fl(amax / 448) (1.0 when zero), codes = encode(fl(x / s)) -- the
@@ -109,6 +119,8 @@ def quantize_col_blocks(x, group_sizes, block_cols: int = 1):
     block_cols = 128: one scale per (token block, 128 columns), the 128x128 block recipe of
     fp8.py:154-176 (quantize_blocks) applied per group token block, repeated in each of the
     block's 128 column slots.
+    scale_pow2: s = pow2_ceil(fl(amax / 448)) (1.0 when zero), a power of two, so x / s is exact
+    and s is one E8M0 byte -- the MXFP8 recipe the block-scaled weight gradient takes.
     """
     x = np.ascontiguousarray(x, dtype=np.float32)
     rows, cols = x.shape
@@ -123,6 +135,8 @@ def quantize_col_blocks(x, group_sizes, block_cols: int = 1):
             if block_cols == 128:
                 amax = np.repeat(amax.reshape(-1, 128).max(axis=1), 128)
             s = np.where(amax > 0, amax / np.float32(E4M3_MAX), np.float32(1.0)).astype(np.float32)
+            if scale_pow2:
+                s = np.where(amax > 0, pow2_ceil(s), np.float32(1.0)).astype(np.float32)
             blocks.append(s)
             codes[sl] = encode(x[sl] / s[None, :])
         off += m

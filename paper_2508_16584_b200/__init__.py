@@ -44,7 +44,7 @@ from .quant import (  # noqa: F401
     quantize_row_tiles,
     route_plan,
 )
-from .wgrad import quantize_col_blocks, wgrad_fp8  # noqa: F401
+from .wgrad import quantize_col_blocks, quantize_col_blocks_mx, wgrad_fp8, wgrad_fp8_mx  # noqa: F401
 from . import tensorio  # noqa: F401
 from . import moe  # noqa: F401
 from .hostpipe import HostBatch, run_host_batches  # noqa: F401

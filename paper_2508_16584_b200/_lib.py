@@ -40,6 +40,9 @@ SIGNATURES = {
                                                 c_i64, c_vp, c_vp, c_vp]),
     "tagg_wgrad_fp8": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_int, c_int, c_int, c_vp, c_vp]),
     "tagg_wgrad_fp8_ex": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_int, c_int, c_int, c_vp, c_u32, c_vp]),
+    "tagg_wgrad_fp8_mx": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_int, c_int, c_int, c_vp, c_vp]),
+    "tagg_quantize_col_blocks_mx": (c_int, [c_vp, c_int, c_i64, c_vp, c_vp, c_i64, c_int, c_vp, c_int, c_vp, c_i64,
+                                            c_vp, c_vp, c_vp, c_vp]),
     "tagg_quantize_col_blocks_ex": (c_int, [c_vp, c_int, c_i64, c_vp, c_vp, c_i64, c_int, c_vp, c_int, c_vp, c_i64,
                                             c_vp, c_vp, c_int, c_vp]),
     "tagg_quantize_blocks": (c_int, [c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp,

@@ -458,6 +458,41 @@ __host__ __device__ constexpr uint32_t idesc_e4m3_f32_ab(uint32_t m, uint32_t n,
          ((m >> 4) << 24);
 }
 
+// ---------------------------------------------------------------- block-scaled MMA (MXFP8)
+// SMEM descriptor without swizzle: 8-row x 16-B core matrices (the tcgen05.cp source of a
+// 32 x 128-bit scale-factor block: rows 16 B apart, LBO = SBO = 128 B).
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;
+}
+// Instruction descriptor, kind::mxf8f6f4.block_scale: E4M3 x E4M3 -> F32, E8M0 scale factors (one
+// per 32 K), both operands MN-major; a_sf_id / b_sf_id pick the scale byte of the TMEM word.
+__host__ __device__ constexpr uint32_t idesc_mx_e4m3_mn(uint32_t m, uint32_t n, uint32_t a_sf_id, uint32_t b_sf_id) {
+  return (b_sf_id << 4) | (1u << 15) | (1u << 16) | ((n >> 3) << 17) | (1u << 23) | ((m >> 4) << 24) |
+         (a_sf_id << 29);
+}
+// D[tmem] (+)= (A * 2^sfa) (B * 2^sfb), scale factors read from TMEM (tcgen05.cp-staged).
+__device__ __forceinline__ void mma_mxf8_cg2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
+// SMEM -> TMEM copy of a 32-lane x 128-bit block, broadcast to the 4 lane quarters; cta_group::2:
+// each CTA of the pair copies its own smem into its own TMEM (issued by the leader).
+__device__ __forceinline__ void utccp_32x128b_warpx4_cg2(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 // ---------------------------------------------------------------- promotion math
 // acc = fl(acc + p*s) on a pair of f32 (one FFMA2; a single rounding).
 __device__ __forceinline__ void ffma2(float& c0, float& c1, float p0, float p1, float s) {

@@ -53,8 +53,17 @@ struct Params {
   const int32_t* group_sizes;
   unsigned long long* trace;  // diagnostics (TAGG_TRACE builds): clock64 stamps of CTAs 0/1
   int G, K, N, KT, NT;        // KT, NT: 256-wide pair tiles (ceil)
-  uint32_t off_a, off_b, off_c, off_s, off_tab, off_bar;
+  uint32_t off_a, off_b, off_c, off_s, off_sf, off_tab, off_bar;
+  CUtensorMap map_sfx, map_sfdy;  // kMx: E8M0 factor blocks, u8 [blocks * 2, 256] / box {256, 2} and {256, 4}
 };
+// MXFP8 mode (TAGG_WGRAD_MX): per stage, this CTA's E8M0 scale factors in the tcgen05.cp source
+// layout -- SFA (its 128 dW rows) 512 B, SFB (the pair tile's 256 columns) 2 x 512 B: byte
+// (16 l + 4 c + j) of a block is the factor of row / column 32 c + l for the j-th 32-token slice
+// (all four the same here: one scale per 128-token block).
+constexpr uint32_t kSfStage = 1536;
+// TMEM: the accumulator [0, 256); stage s's factors at 256 + 16 s: SFA 4 columns, SFB 8 columns
+// (row / column 32 c + l in lane l (+ 32 q, broadcast), column c, byte j -- tools/micro/mxf8.cu).
+constexpr uint32_t kTmemSf0 = 256;
 
 // Diagnostics: the same event layout as the forward kernel's trace (tools/trace_wg.py).
 enum WgEv { kWgMmaTempty = 0, kWgMmaFull, kWgMmaIssued, kWgProdEmpty, kWgPromoFull, kWgPromoFreed, kWgPromoDone,
@@ -72,7 +81,14 @@ __device__ __forceinline__ void wg_stamp(unsigned long long* tr, int ev, uint32_
 // tagg_quantize_col_blocks_ex, block_cols = 128): a thread's 128 columns are one block, so its
 // promotion is s = fl(sx * sdy) once per token block and one FFMA2 per element pair -- the forward
 // kernel's promotion -- instead of an FMUL2 and an FFMA2.
-template <bool kDyBlock>
+// kMx (TAGG_WGRAD_MX): sx and sdy are powers of two (the MXFP8 recipe, quantize_col_blocks with
+// TAGG_QCB_SCALE_POW2).  The tensor core applies them as E8M0 block scales
+// (tcgen05.mma kind::mxf8f6f4.block_scale) and accumulates the group's whole token range in one
+// TMEM accumulator: no per-block promotion.  The factors come pre-laid-out by the quantizer
+// (tagg_quantize_col_blocks_mx: E8M0 bytes in the tcgen05.cp source layout) and ride with each
+// stage's operands on the same TMA barrier; the eight promotion warps only drain the finished tile
+// and store it.
+template <bool kDyBlock, bool kMx>
 __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -148,9 +164,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
         const int kr = k0 + 128 * rank, nr = n0 + 128 * rank;  // this CTA's K rows, B columns
         const int m = tab_m[g], off = tab_off[g], tb0 = tab_tb[g];
         for (int j = 0; j * BT < m; ++j) {
-          // scales of this token block: sx[tb][kr..+128), sdy[tb][n0..+256)
-          mbar_wait_addr(smem_u32(&sempty[sring]), sph ^ 1);
-          if (lane == 0) {
+          // scales of this token block: sx[tb][kr..+128), sdy[tb][n0..+256) (kMx: E8M0 factor blocks
+          // loaded with the operands below instead)
+          if (!kMx) mbar_wait_addr(smem_u32(&sempty[sring]), sph ^ 1);
+          if (!kMx && lane == 0) {
             const uint32_t dst = sS0 + sring * kScaleSlot;
             const int64_t tb = tb0 + j;
             const uint32_t nsx = kr < p.K ? 512u : 0u;
@@ -159,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
             if (nsx) bulk_load_1d_addr(dst, p.sx + tb * p.K + kr, nsx, smem_u32(&sfull[sring]));
             bulk_load_1d_addr(dst + 512, p.sdy + tb * p.N + n0, nsdy, smem_u32(&sfull[sring]));
           }
-          if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
+          if (!kMx && ++sring == kScaleRing) { sring = 0; sph ^= 1; }
           // operands
           mbar_wait_addr(smem_u32(&empty[stage]), phase ^ 1);
           if (lane == 0) wg_stamp(p.trace, kWgProdEmpty, piter);
@@ -181,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           if (lane == 0) {
             const uint32_t fb = smem_u32(&full[stage]);
             const int lg = res == BT ? 7 : 31 - __clz(res), d = 1 << lg;
-            const uint32_t bytes = (res == BT) ? 2u * (kStageA + kStageB) : 2u * 4u * d * 128u;
+            const uint32_t bytes = ((res == BT) ? 2u * (kStageA + kStageB) : 2u * 4u * d * 128u) + (kMx ? 2u * kSfStage : 0u);
             if (rank == 0) {
               mbar_arrive_expect_tx_addr(fb, bytes);
             } else if (res < BT) {
@@ -197,6 +214,14 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
               tma_load_2d_u32<2>(&p.map_x[lg], fb, a_dst + (res - d) * 128u, kr, row0 + res - d);
               tma_load_2d_u32<2>(&p.map_dy[lg], fb, b_dst + (res - d) * 128u, nr, row0 + res - d);
             }
+            if constexpr (kMx) {
+              // this CTA's SFA block (its 128 dW rows) and the tile's two SFB blocks (256 columns):
+              // 512-B blocks [token block][128 columns], two 256-B rows each
+              const uint32_t sfd = smem_u32(smem + p.off_sf) + stage * kSfStage;
+              const int64_t tb = tb0 + j;
+              tma_load_2d_u32<2>(&p.map_sfx, fb, sfd, 0, static_cast<int32_t>((tb * (p.K >> 7) + (kr >> 7)) * 2));
+              tma_load_2d_u32<2>(&p.map_sfdy, fb, sfd + 512u, 0, static_cast<int32_t>((tb * (p.N >> 7) + (n0 >> 7)) * 2));
+            }
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -208,6 +233,46 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       __syncwarp();
+    } else if (warp == 1 && rank == 0 && kMx) {
+      // ====================================================== MMA, MXFP8 (leader)
+      // One accumulator per tile: the group's token blocks accumulate in TMEM with their E8M0
+      // factors applied by the tensor core; each block's factors are copied smem -> TMEM right
+      // before its MMAs (tcgen05.cp and tcgen05.mma execute in issue order).
+      const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
+      const uint64_t a0 = umma_desc_sw128(smem_u32(smem + p.off_a), kStageA, 1024);
+      const uint64_t b0 = umma_desc_sw128(smem_u32(smem + p.off_b), kStageB, 1024);
+      const uint32_t sF0 = smem_u32(smem + p.off_sf);
+      uint32_t stage = 0, phase = 0, accph = 0, miter = 0;
+      for (int t = cid; t < tiles; t += nclusters) {
+        const int m = tab_m[t / (p.KT * p.NT)];
+        if (m <= 0) continue;  // an empty group's tile is stored as zeros, with no MMA
+        const int nb = (m + BT - 1) / BT;
+        for (int j = 0; j < nb; ++j) {
+          mbar_wait_addr(smem_u32(&full[stage]), phase);  // operands and their E8M0 factors
+          if (lane == 0) wg_stamp(p.trace, kWgMmaFull, miter);
+          if (j == 0) mbar_wait_addr(smem_u32(&tempty[0]), accph ^ 1);  // the previous tile is drained
+          if (lane == 0) wg_stamp(p.trace, kWgMmaTempty, miter);
+          tc_fence_after();
+          const uint64_t ad = a0 + ((stage * kStageA) >> 4), bd = b0 + ((stage * kStageB) >> 4);
+          if (elect_one()) {
+            const uint32_t tsf = tmem_base + kTmemSf0 + 16u * stage, sf = sF0 + stage * kSfStage;
+            utccp_32x128b_warpx4_cg2(tsf, umma_desc_noswz(sf, 128, 128));
+            utccp_32x128b_warpx4_cg2(tsf + 4, umma_desc_noswz(sf + 512, 128, 128));
+            utccp_32x128b_warpx4_cg2(tsf + 8, umma_desc_noswz(sf + 1024, 128, 128));
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_mxf8_cg2(tmem_base, ad + static_cast<uint64_t>(k * 256), bd + static_cast<uint64_t>(k * 256),
+                           idesc_mx_e4m3_mn(256, 256, k, k), tsf, tsf + 4, (j > 0 || k > 0) ? 1u : 0u);
+            mma_commit_addr<2>(smem_u32(&empty[stage]));
+            if (j + 1 == nb) mma_commit_addr<2>(smem_u32(&tfull[0]));
+          }
+          __syncwarp();
+          if (lane == 0) wg_stamp(p.trace, kWgMmaIssued, miter);
+          ++miter;
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        accph ^= 1;
+      }
     } else if (warp == 1 && rank == 0) {
       // ====================================================== MMA (leader, whole warp, elected issue)
       const uint32_t tmem_base = ld_shared_u32(smem_u32(tmem_slot));
@@ -256,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     const uint32_t sfull0 = opaque_u32(smem_u32(&sfull[0])), sempty0 = opaque_u32(smem_u32(&sempty[0]));
     uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0, kiter = 0, tiles_done = 0;
     const bool tr = p.trace != nullptr && pw == 0 && lane == 0;
+    uint32_t mx_ph = 0;  // kMx: parity of the single accumulator's handoffs
     for (int t = cid; t < tiles; t += nclusters) {
       const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
       const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
@@ -264,6 +330,37 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
       float acc[128];
 #pragma unroll
       for (int i = 0; i < 128; ++i) acc[i] = 0.0f;
+      if constexpr (kMx) {
+        // the finished tile: this thread's row, its 128 columns, already scaled; the accumulator
+        // goes back to the MMA as soon as the last chunk has landed, before the epilogue
+        if (m > 0) {
+          mbar_wait_addr(tfull0, mx_ph);
+          if (tr) wg_stamp(p.trace, kWgPromoFull, tiles_done);
+          tc_fence_after();
+          const uint32_t taddr = tmem_base + t_lane + 128u * half;
+          uint32_t va[32], vb[32];
+          tmem_ld_32x32b_x32(taddr, va);
+          tmem_ld_32x32b_x32(taddr + 32, vb);
+          tmem_wait_ld_dep2(va, vb);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(va[i]);
+          tmem_ld_32x32b_x32(taddr + 64, va);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[32 + i] = __uint_as_float(vb[i]);
+          tmem_ld_32x32b_x32(taddr + 96, vb);
+          tmem_wait_ld_dep2(va, vb);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader_addr(tempty0);
+          if (tr) wg_stamp(p.trace, kWgPromoFreed, tiles_done);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            acc[64 + i] = __uint_as_float(va[i]);
+            acc[96 + i] = __uint_as_float(vb[i]);
+          }
+          mx_ph ^= 1;
+        }
+      } else
       for (int j = 0; j * BT < m; ++j) {
         mbar_wait_addr(sfull0 + 8 * sring, sph);
         if (tr) wg_stamp(p.trace, kWgPromoSfull, kiter);
@@ -360,13 +457,22 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
   }
 }
 
+// The MXFP8 scale: the smallest power of two >= q (at least 2^-126), i.e. one E8M0 byte
+// ((bits >> 23) & 0xFF); x / s is then exact (oracle/fp8.py: pow2_ceil).
+__device__ __forceinline__ float pow2_ceil(float q) {
+  uint32_t b = __float_as_uint(q);
+  if (b & 0x7FFFFFu) b = (b & 0xFF800000u) + 0x800000u;
+  return __uint_as_float(max(b, 0x00800000u));
+}
+
 // Per-group 128x1 column-block quantizer: CTA (row block y, column chunk x), thread =
 // one column; pass 1 takes the block's amax, pass 2 (L2-resident re-read) quantizes.
 template <bool kBf16>
 __global__ void __launch_bounds__(128) quantize_col_blocks_kernel(const void* __restrict__ x, int64_t ldx, int cols,
                                                                   const int32_t* __restrict__ group_sizes, int G,
                                                                   uint8_t* __restrict__ codes, int64_t ldc,
-                                                                  float* __restrict__ scales, int32_t* err) {
+                                                                  float* __restrict__ scales, int32_t* err,
+                                                                  int pow2) {
   __shared__ int32_t s_row0, s_rows, s_tb;
   if (threadIdx.x < 32) {
     // which (group, block) is this CTA's: walk the group table
@@ -420,7 +526,8 @@ __global__ void __launch_bounds__(128) quantize_col_blocks_kernel(const void* __
     bad |= !(m <= 3.402823466e38f);
     amax = fmaxf(amax, m);
   }
-  const float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  float s = amax > 0.0f ? __fdiv_rn(amax, 448.0f) : 1.0f;
+  if (pow2 && amax > 0.0f) s = pow2_ceil(s);
   scales[static_cast<int64_t>(s_tb) * cols + c] = s;
   for (int i = 0; i < rows; i += 2) {
     const float v0 = __fdiv_rn(ld(row0 + i), s);
@@ -513,7 +620,8 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
                                                                    uint8_t* __restrict__ codes, int64_t ldc,
                                                                    float* __restrict__ scales, int32_t* err,
                                                                    const int32_t* __restrict__ index,
-                                                                   const float* __restrict__ row_weights) {
+                                                                   const float* __restrict__ row_weights, int pow2,
+                                                                   uint32_t* __restrict__ sf_out) {
   __shared__ int32_t s_row0, s_rows, s_tb;
   __shared__ __align__(16) uint32_t s_part[2][8][128];  // per-warp column maxima (|x| bits)
   __shared__ __align__(16) float s_scale[2][128];
@@ -637,15 +745,20 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
     }
     if (t < 128) {
       const float am = __uint_as_float(cm);
-      const float sc = am > 0.0f ? __fdiv_rn(am, 448.0f) : 1.0f;
+      float sc = am > 0.0f ? __fdiv_rn(am, 448.0f) : 1.0f;
+      if (pow2 && am > 0.0f) sc = pow2_ceil(sc);
       const float rd = __frcp_rd(sc);
       s_scale[buf][t] = sc;
       s_rlo[buf][t] = rd;
-      // >= (1/s)(1 + 2^-22): RU(1/s) raised by two ulps (or 1/s overflowing to inf)
+      // >= (1/s)(1 + 2^-22): RU(1/s) raised by two ulps (or 1/s overflowing to inf).  A power-of-two
+      // s has an exact reciprocal (x * 1/s is x / s), so both bounds are the same there.
       const float ru = __frcp_ru(sc);
-      s_rhi[buf][t] = isinf(ru) ? ru : __uint_as_float(__float_as_uint(ru) + 2u);
+      s_rhi[buf][t] = pow2 ? rd : (isinf(ru) ? ru : __uint_as_float(__float_as_uint(ru) + 2u));
       const int c = cb * 128 + t;
       if (c < cols) scales[tb * cols + c] = sc;
+      // MXFP8: the E8M0 byte of this column's scale in the tcgen05.cp source block of
+      // (token block, 128 columns): byte 16 l + 4 c + j for column 32 c + l, every 32-token slice j
+      if (sf_out) sf_out[(tb * (cols >> 7) + cb) * 128 + (t & 31) * 4 + (t >> 5)] = ((__float_as_uint(sc) >> 23) & 0xFFu) * 0x01010101u;
     }
     __syncthreads();
     {
@@ -725,7 +838,7 @@ extern "C" int64_t tagg_token_blocks_bound(int64_t m_alloc, int G) {
 static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
                                     const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
                                     int32_t* err_flag, const int32_t* index, const float* row_weights, void* stream,
-                                    int block_cols = 1);
+                                    int block_cols = 1, int pow2 = 0, uint32_t* sf = nullptr);
 
 extern "C" int tagg_quantize_col_blocks(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
                                         const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
@@ -750,6 +863,8 @@ extern "C" int tagg_quantize_col_blocks_ex(const void* x, int x_dtype, int64_t l
                                            const float* row_weights, int64_t rows, int cols,
                                            const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
                                            int32_t* err_flag, int block_cols, void* stream) {
+  const int pow2 = (block_cols & TAGG_QCB_SCALE_POW2) ? 1 : 0;
+  block_cols &= ~TAGG_QCB_SCALE_POW2;
   if (block_cols != 1 && block_cols != 128) return TAGG_ERR_CONFIG;
   if (block_cols == 128 && (cols % 128 || (reinterpret_cast<uintptr_t>(x) % 16) ||
                             ((ldx * (x_dtype == TAGG_DTYPE_BF16 ? 2 : 4)) % 16) ||
@@ -758,13 +873,24 @@ extern "C" int tagg_quantize_col_blocks_ex(const void* x, int x_dtype, int64_t l
     return TAGG_ERR_ALIGNMENT;  // the 128-column block form is the vector kernel only
   if (rows > 0 && index == nullptr && row_weights != nullptr) return TAGG_ERR_SHAPE;
   return quantize_col_blocks_impl(x, x_dtype, rows, cols, ldx, group_sizes, G, codes, ldc, scales, err_flag, index,
-                                  row_weights, stream, block_cols);
+                                  row_weights, stream, block_cols, pow2);
+}
+
+extern "C" int tagg_quantize_col_blocks_mx(const void* x, int x_dtype, int64_t ldx, const int32_t* index,
+                                           const float* row_weights, int64_t rows, int cols,
+                                           const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
+                                           void* sf, int32_t* err_flag, void* stream) {
+  if (!sf) return TAGG_ERR_SHAPE;
+  if (cols % 128 || (reinterpret_cast<uintptr_t>(sf) % 16)) return TAGG_ERR_ALIGNMENT;
+  if (rows > 0 && index == nullptr && row_weights != nullptr) return TAGG_ERR_SHAPE;
+  return quantize_col_blocks_impl(x, x_dtype, rows, cols, ldx, group_sizes, G, codes, ldc, scales, err_flag, index,
+                                  row_weights, stream, 1, 1, static_cast<uint32_t*>(sf));
 }
 
 static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc, int cols, int64_t ldx,
                                     const int32_t* group_sizes, int G, void* codes, int64_t ldc, float* scales,
                                     int32_t* err_flag, const int32_t* index, const float* row_weights, void* stream,
-                                    int block_cols) {
+                                    int block_cols, int pow2, uint32_t* sf) {
   if (x_dtype != TAGG_DTYPE_BF16 && x_dtype != TAGG_DTYPE_F32) return TAGG_ERR_CONFIG;
   if (G < 1 || cols < 1 || m_alloc < 0 || ldx < cols || ldc < cols) return TAGG_ERR_SHAPE;
   if (m_alloc == 0) return TAGG_OK;
@@ -775,11 +901,12 @@ static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc,
   const int esz = x_dtype == TAGG_DTYPE_BF16 ? 2 : 4;
   const bool v8 = cols % 8 == 0 && !(reinterpret_cast<uintptr_t>(x) % 16) && !((ldx * esz) % 16) &&
                   !(reinterpret_cast<uintptr_t>(codes) % 8) && !(ldc % 8) && !(reinterpret_cast<uintptr_t>(scales) % 16);
+  if (sf && (!v8 || cols % 128)) return TAGG_ERR_ALIGNMENT;  // the E8M0 blocks come from the vector kernel
   if (v8) {
     const dim3 gt(static_cast<unsigned>(tb));
     auto launch = [&](auto kern) {
       kern<<<gt, 256, 0, st>>>(x, ldx, cols, group_sizes, G, static_cast<uint8_t*>(codes), ldc, scales, err_flag, index,
-                               row_weights);
+                               row_weights, pow2, sf);
     };
     const bool bf16 = x_dtype == TAGG_DTYPE_BF16, w = row_weights != nullptr, b128 = block_cols == 128;
     using namespace wg;
@@ -795,10 +922,10 @@ static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc,
   const dim3 grid(static_cast<unsigned>((cols + 127) / 128), static_cast<unsigned>(tb));
   if (x_dtype == TAGG_DTYPE_BF16)
     wg::quantize_col_blocks_kernel<true><<<grid, 128, 0, st>>>(x, ldx, cols, group_sizes, G,
-                                                               static_cast<uint8_t*>(codes), ldc, scales, err_flag);
+                                                               static_cast<uint8_t*>(codes), ldc, scales, err_flag, pow2);
   else
     wg::quantize_col_blocks_kernel<false><<<grid, 128, 0, st>>>(x, ldx, cols, group_sizes, G,
-                                                                static_cast<uint8_t*>(codes), ldc, scales, err_flag);
+                                                                static_cast<uint8_t*>(codes), ldc, scales, err_flag, pow2);
   return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
 }
 
@@ -807,15 +934,36 @@ extern "C" int tagg_wgrad_fp8(const void* x, const float* sx, const void* dy, co
   return tagg_wgrad_fp8_ex(x, sx, dy, sdy, m_alloc, group_sizes, G, K, N, dw, 0u, stream);
 }
 
+static int wgrad_launch(const void* x, const float* sx, const void* dy, const float* sdy, const void* x_sf,
+                        const void* dy_sf, int64_t m_alloc, const int32_t* group_sizes, int G, int K, int N, void* dw,
+                        uint32_t flags, void* stream);
+
 extern "C" int tagg_wgrad_fp8_ex(const void* x, const float* sx, const void* dy, const float* sdy, int64_t m_alloc,
                                  const int32_t* group_sizes, int G, int K, int N, void* dw, uint32_t flags,
                                  void* stream) {
+  if (flags & TAGG_WGRAD_MX) return TAGG_ERR_CONFIG;  // the MXFP8 path takes E8M0 factor blocks: tagg_wgrad_fp8_mx
+  if (!sx || !sdy) return TAGG_ERR_SHAPE;
+  return wgrad_launch(x, sx, dy, sdy, nullptr, nullptr, m_alloc, group_sizes, G, K, N, dw, flags, stream);
+}
+
+extern "C" int tagg_wgrad_fp8_mx(const void* x, const void* x_sf, const void* dy, const void* dy_sf, int64_t m_alloc,
+                                 const int32_t* group_sizes, int G, int K, int N, void* dw, void* stream) {
+  if (!x_sf || !dy_sf) return TAGG_ERR_SHAPE;
+  return wgrad_launch(x, nullptr, dy, nullptr, x_sf, dy_sf, m_alloc, group_sizes, G, K, N, dw, TAGG_WGRAD_MX, stream);
+}
+
+static int wgrad_launch(const void* x, const float* sx, const void* dy, const float* sdy, const void* x_sf,
+                        const void* dy_sf, int64_t m_alloc, const int32_t* group_sizes, int G, int K, int N, void* dw,
+                        uint32_t flags, void* stream) {
   using namespace tagg::wg;
+  const bool mx = (flags & TAGG_WGRAD_MX) != 0;
   if (G < 1 || K < 128 || N < 128 || K % 128 || N % 128) return TAGG_ERR_CONFIG;
   if (m_alloc < 0) return TAGG_ERR_SHAPE;
-  if (!x || !sx || !dy || !sdy || !group_sizes || !dw) return TAGG_ERR_SHAPE;
+  if (!x || !dy || !group_sizes || !dw) return TAGG_ERR_SHAPE;
   auto mis = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) != 0; };
-  if (mis(x) || mis(dy) || mis(dw) || mis(sx) || mis(sdy)) return TAGG_ERR_ALIGNMENT;
+  if (mis(x) || mis(dy) || mis(dw) || (sx && mis(sx)) || (sdy && mis(sdy)) || (x_sf && mis(x_sf)) ||
+      (dy_sf && mis(dy_sf)))
+    return TAGG_ERR_ALIGNMENT;
   if (static_cast<int64_t>(G) * K >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
   const int sms = sm_count();
   if (sms <= 0) return TAGG_ERR_CUDA;
@@ -839,6 +987,17 @@ extern "C" int tagg_wgrad_fp8_ex(const void* x, const float* sx, const void* dy,
     if (!encode_map(&p.map_dw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dw, d, s, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return TAGG_ERR_CUDA;
   }
+  if (mx) {
+    // factor blocks: [token blocks][columns / 128] blocks of 512 B, viewed as 256-B rows
+    const int64_t tbb = tagg_token_blocks_bound(m_alloc, G);
+    const uint64_t st[1] = {256};
+    const uint64_t dfx[2] = {256, static_cast<uint64_t>(std::max<int64_t>(tbb, 1) * (K / 128) * 2)};
+    const uint64_t dfd[2] = {256, static_cast<uint64_t>(std::max<int64_t>(tbb, 1) * (N / 128) * 2)};
+    const uint32_t bx[2] = {256, 2}, bd[2] = {256, 4};
+    if (!encode_map(&p.map_sfx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, x_sf, dfx, st, bx, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode_map(&p.map_sfdy, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, dy_sf, dfd, st, bd, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return TAGG_ERR_CUDA;
+  }
   p.sx = sx;
   p.sdy = sdy;
   p.group_sizes = group_sizes;
@@ -852,18 +1011,20 @@ extern "C" int tagg_wgrad_fp8_ex(const void* x, const float* sx, const void* dy,
   p.off_b = p.off_a + kStages * kStageA;
   p.off_c = p.off_b + kStages * kStageB;
   p.off_s = p.off_c + 4 * kChunkC;
-  p.off_tab = p.off_s + kScaleRing * kScaleSlot;
+  p.off_sf = p.off_s + kScaleRing * kScaleSlot;
+  p.off_tab = p.off_sf + kStages * kSfStage;
   const uint32_t tab = static_cast<uint32_t>(((3 * G * 4) + 15) & ~15);
   p.off_bar = p.off_tab + tab;
   const uint32_t smem = p.off_bar + (2 * kStages + 2 * kNumAcc + 2 * kScaleRing) * 8 + 16 + 1024;
   if (smem > 232448) return TAGG_ERR_UNSUPPORTED;
-  const bool dy_block = (flags & TAGG_WGRAD_DY_BLOCK128) != 0;
-  auto kern = dy_block ? wgrad_kernel<true> : wgrad_kernel<false>;
-  static bool configured[2] = {false, false};
-  if (!configured[dy_block]) {
+  const bool dy_block = !mx && (flags & TAGG_WGRAD_DY_BLOCK128) != 0;
+  const int variant = mx ? 2 : (dy_block ? 1 : 0);
+  auto kern = mx ? wgrad_kernel<false, true> : (dy_block ? wgrad_kernel<true, false> : wgrad_kernel<false, false>);
+  static bool configured[3] = {false, false, false};
+  if (!configured[variant]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448) != cudaSuccess)
       return TAGG_ERR_CUDA;
-    configured[dy_block] = true;
+    configured[variant] = true;
   }
   const int64_t tiles = static_cast<int64_t>(G) * p.KT * p.NT;
   const int grid = static_cast<int>(std::min<int64_t>(sms / 2, tiles)) * 2;

@@ -150,52 +150,83 @@ def test_col_block_gather_equals_quantizing_the_gathered_copy(dtype):
     assert torch.equal(plain_c, want_pc) and torch.equal(plain_s[:tb], want_ps[:tb])
 
 
+def _sf_blocks(scales):
+    """The E8M0 factor blocks tagg_quantize_col_blocks_mx lays out: per (token block, 128
+    columns) byte 16 l + 4 c + j = the exponent byte of column 32 c + l's scale (j = 0..3)."""
+    tb, cols = scales.shape
+    e = ((scales.view(np.uint32) >> 23) & 0xFF).astype(np.uint8).reshape(tb, cols // 128, 4, 32)  # [tb, blk, c, l]
+    return np.repeat(e.transpose(0, 1, 3, 2)[..., None], 4, axis=-1).reshape(tb, cols // 128, 512)
+
+
 @pytest.mark.parametrize("sizes", [(200,), (1, 0, 129, 255, 384)])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("gather", [False, True])
-def test_quantize_col_blocks_128_column_blocks_is_bit_exact(sizes, dtype, gather):
-    """block_cols=128: one scale per (group token block, 128 columns), the 128x128 block recipe
-    of fp8.py:154-176, against oracle/fp8.quantize_col_blocks(block_cols=128)."""
-    x, _ = _data(sizes, 384, 256, 2)
+def test_quantize_col_blocks_mx_is_bit_exact(sizes, dtype, gather):
+    """The MXFP8 recipe: s = pow2_ceil(fl(amax / 448)), codes = e4m3(x / s) with an exact
+    quotient -- bit-exact against oracle/fp8.quantize_col_blocks(..., scale_pow2=True) --, every
+    scale a power of two, and the E8M0 factor blocks in the tcgen05.cp source layout.  The
+    plain entry point with scale_pow2 gives the same codes and scales."""
+    x, _ = _data(sizes, 256, 128, 11)
     m = sum(sizes)
     xt = torch.from_numpy(x).to(DEV).to(dtype)
     gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
-    if gather:
-        perm = torch.randperm(m, generator=torch.Generator().manual_seed(m)).to(torch.int32)
-        w = torch.rand(m, generator=torch.Generator().manual_seed(m + 1))
-        src = torch.empty_like(xt)
-        src[perm.to(torch.int64).to(DEV)] = xt  # token order: grouped row r = w[r] * src[perm[r]]
-        codes, scales = tg.quantize_col_blocks(src, gs, index=perm.to(DEV), row_weights=w.to(DEV), block_cols=128,
-                                               check=True)
-        ref = (w.numpy()[:, None] * xt.float().cpu().numpy()).astype(np.float32)
-    else:
-        codes, scales = tg.quantize_col_blocks(xt, gs, block_cols=128, check=True)
-        ref = xt.float().cpu().numpy()
+    perm = torch.randperm(m, generator=torch.Generator().manual_seed(3)).to(DEV) if gather else None
+    codes, scales, sf = tg.quantize_col_blocks_mx(xt, gs, check=True, index=perm)
+    codes2, scales2 = tg.quantize_col_blocks(xt, gs, index=perm, scale_pow2=True)
     torch.cuda.synchronize()
-    want_c, want_s = ofp8.quantize_col_blocks(ref, sizes, block_cols=128)
-    np.testing.assert_array_equal(codes.cpu().numpy(), want_c)
+    ref_x = xt.float()[perm].cpu().numpy() if gather else xt.float().cpu().numpy()
+    want_c, want_s = ofp8.quantize_col_blocks(ref_x, sizes, scale_pow2=True)
     tb = want_s.shape[0]
-    np.testing.assert_array_equal(scales[:tb].cpu().numpy().view(np.uint32), want_s.view(np.uint32))
+    np.testing.assert_array_equal(codes.cpu().numpy(), want_c)
+    got_s = scales[:tb].cpu().numpy()
+    np.testing.assert_array_equal(got_s.view(np.uint32), want_s.view(np.uint32))
+    assert np.all((got_s.view(np.uint32) & 0x7FFFFF) == 0), "every scale is a power of two"
+    np.testing.assert_array_equal(sf[:tb].cpu().numpy(), _sf_blocks(want_s))
+    np.testing.assert_array_equal(codes2.cpu().numpy(), want_c)
+    np.testing.assert_array_equal(scales2[:tb].cpu().numpy().view(np.uint32), want_s.view(np.uint32))
 
 
 @pytest.mark.parametrize("sizes,k,n", [
+    ((128,), 128, 128),
     ((300, 0, 1, 77, 256), 256, 384),
-    (tuple(range(1, 128, 9)), 128, 256),
+    (tuple(range(1, 128, 9)), 128, 256),       # every residue class, ragged reduction
     ((1000, 513), 384, 256),
+    ((0, 0, 700), 256, 256),                   # leading empty groups: their tiles store zeros
 ])
-def test_wgrad_dy_block128_matches_oracle(sizes, k, n):
-    """TAGG_WGRAD_DY_BLOCK128 (dY with 128x128 block scales, one FFMA2 per pair) against the
-    C oracle on the same operands (the oracle reads the per-column scale slots, which repeat
-    the block scale)."""
-    x, dy = _data(sizes, k, n, sum(sizes) + 5)
+def test_wgrad_mx_matches_oracle(sizes, k, n):
+    """wgrad_fp8_mx: power-of-two scales applied by the tensor core as E8M0 block scales
+    (kind::mxf8f6f4.block_scale) with each tile's whole token range accumulated in TMEM, against
+    the C oracle (per-block promotion in fp32) on the same operands: the same real sum, rounded
+    differently in fp32, so within the bf16 tolerance."""
+    x, dy = _data(sizes, k, n, sum(sizes) + 9)
     gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
-    xc, xs = tg.quantize_col_blocks(torch.from_numpy(x).to(DEV), gs)
-    dc, ds = tg.quantize_col_blocks(torch.from_numpy(dy).to(DEV), gs, block_cols=128)
-    dw = tg.wgrad_fp8(xc, xs, dc, ds, gs, dy_block128=True)
+    xc, xs, xf = tg.quantize_col_blocks_mx(torch.from_numpy(x).to(DEV), gs)
+    dc, ds, df = tg.quantize_col_blocks_mx(torch.from_numpy(dy).to(DEV), gs)
+    dw = tg.wgrad_fp8_mx(xc, xf, dc, df, gs)
     torch.cuda.synchronize()
     tb = sum(-(-s // 128) for s in sizes)
     want = orc.wgrad(xc.cpu().numpy(), xs[:tb].cpu().numpy(), dc.cpu().numpy(), ds[:tb].cpu().numpy(), sizes,
                      threads=8)
     got = dw.view(torch.int16).cpu().numpy().view(np.uint16)
-    for g in range(len(sizes)):
-        assert_parity(got[g], want[g], label=f"group {g}")
+    for g, m in enumerate(sizes):
+        if m == 0:
+            assert np.all(got[g] == 0), "an empty group's gradient is zero"
+        else:
+            assert_parity(got[g], want[g], label=f"mx group {g} (M_g={m})")
+
+
+def test_wgrad_mx_never_reads_the_next_group():
+    """MXFP8 path: poisoning the rows after a short group leaves its gradient unchanged."""
+    sizes = (70, 300)
+    k, n = 128, 256
+    x, dy = _data(sizes, k, n, 6)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    xc, _, xf = tg.quantize_col_blocks_mx(torch.from_numpy(x).to(DEV), gs)
+    dc, _, df = tg.quantize_col_blocks_mx(torch.from_numpy(dy).to(DEV), gs)
+    base = tg.wgrad_fp8_mx(xc, xf, dc, df, gs)[0].clone()
+    xc2, dc2 = xc.clone(), dc.clone()
+    xc2[70:198] = 0x7E
+    dc2[70:198] = 0x7E
+    again = tg.wgrad_fp8_mx(xc2, xf, dc2, df, gs)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(base.view(torch.int16), again.view(torch.int16))
