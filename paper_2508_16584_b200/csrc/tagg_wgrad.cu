@@ -36,7 +36,10 @@ constexpr int BT = 128;                 // tokens per k-block
 constexpr int kThreads = 384;
 constexpr int kPromoWarps = 8;
 constexpr int kNumAcc = 2;              // TMEM buffers of 256 columns
-constexpr int kStages = 4;
+#ifndef WG_STAGES
+#define WG_STAGES 4
+#endif
+constexpr int kStages = WG_STAGES;
 constexpr int kScaleRing = 8;           // k-block scale slots: sx 128 + sdy 256 floats
 constexpr uint32_t kStageA = BT * 128;  // 128 token rows x this CTA's 128 K columns
 constexpr uint32_t kStageB = BT * 128;  // 128 token rows x this CTA's 128 N columns
@@ -214,14 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
               tma_load_2d_u32<2>(&p.map_x[lg], fb, a_dst + (res - d) * 128u, kr, row0 + res - d);
               tma_load_2d_u32<2>(&p.map_dy[lg], fb, b_dst + (res - d) * 128u, nr, row0 + res - d);
             }
-            if constexpr (kMx) {
-              // this CTA's SFA block (its 128 dW rows) and the tile's two SFB blocks (256 columns):
-              // 512-B blocks [token block][128 columns], two 256-B rows each
-              const uint32_t sfd = smem_u32(smem + p.off_sf) + stage * kSfStage;
-              const int64_t tb = tb0 + j;
-              tma_load_2d_u32<2>(&p.map_sfx, fb, sfd, 0, static_cast<int32_t>((tb * (p.K >> 7) + (kr >> 7)) * 2));
-              tma_load_2d_u32<2>(&p.map_sfdy, fb, sfd + 512u, 0, static_cast<int32_t>((tb * (p.N >> 7) + (n0 >> 7)) * 2));
-            }
+
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -233,6 +229,32 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       __syncwarp();
+    } else if (kMx && warp == 3) {
+      // ====================================================== E8M0 factor loads (kMx, both CTAs)
+      // The stage's factor blocks ride on its full barrier (the leader's expect_tx counts them); a
+      // warp of their own keeps their TMA issues off the operand producer's path.
+      uint32_t stage = 0, phase = 0;
+      const uint32_t sf0 = smem_u32(smem + p.off_sf);
+      for (int t = cid; t < tiles; t += nclusters) {
+        const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
+        const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
+        const int kr = k0 + 128 * rank;
+        const int m = tab_m[g], tb0 = tab_tb[g];
+        for (int j = 0; j * BT < m; ++j) {
+          mbar_wait_addr(smem_u32(&empty[stage]), phase ^ 1);
+          if (elect_one()) {
+            // this CTA's SFA block (its 128 dW rows) and the tile's two SFB blocks (256 columns):
+            // 512-B blocks [token block][128 columns], two 256-B rows each
+            const uint32_t fb = smem_u32(&full[stage]), sfd = sf0 + stage * kSfStage;
+            const int64_t tb = tb0 + j;
+            tma_load_2d_u32<2>(&p.map_sfx, fb, sfd, 0, static_cast<int32_t>((tb * (p.K >> 7) + (kr >> 7)) * 2));
+            tma_load_2d_u32<2>(&p.map_sfdy, fb, sfd + 512u, 0,
+                               static_cast<int32_t>((tb * (p.N >> 7) + (n0 >> 7)) * 2));
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
     } else if (warp == 1 && rank == 0 && kMx) {
       // ====================================================== MMA, MXFP8 (leader)
       // One accumulator per tile: the group's token blocks accumulate in TMEM with their E8M0
