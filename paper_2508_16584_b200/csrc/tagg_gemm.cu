@@ -48,6 +48,9 @@
 #include "tagg_host.h"
 #include "tagg_ptx.cuh"
 
+#ifndef TAGG_SPLIT_B
+#define TAGG_SPLIT_B 1
+#endif
 #ifndef TAGG_DRAIN_MODE
 #define TAGG_DRAIN_MODE 1
 #endif
@@ -297,6 +300,7 @@ __device__ __forceinline__ int cluster_index() {
 template <int kCG, int kBN, bool kExact, bool kSwizzleC>
 __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_constant__ Params p) {
   using C = Cfg<kCG, kBN>;
+  constexpr bool kSplitB = TAGG_SPLIT_B != 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5;
@@ -460,10 +464,12 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
                 tma_load_2d_hint<kCG>(&p.tmap_a, fb, sA0 + stage * kStageBytesA, kb * BK, T.row0, p.l2_a);
               else
                 tma_load_2d_u32<kCG>(&p.tmap_a, fb, sA0 + stage * kStageBytesA, kb * BK, T.row0);
-              if (p.l2_b)
-                tma_load_3d_hint<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb, p.l2_b);
-              else
-                tma_load_3d_u32<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb);
+              if (!kSplitB) {
+                if (p.l2_b)
+                  tma_load_3d_hint<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb, p.l2_b);
+                else
+                  tma_load_3d_u32<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb);
+              }
             }
           }
           __syncwarp();
@@ -480,6 +486,35 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       }
     }
     __syncwarp();
+  } else if (kSplitB && warp == 3) {
+    // ========================================================== B loader
+    // The B k-blocks of every stage, issued from their own warp: a TMA issue holds the issuing
+    // warp for a while, and one warp issuing both boxes per k-block was measured to pace the
+    // pipeline (the weight-gradient kernel's factor loads: +13% when moved off its producer).
+    // The bytes count on the same full barrier (the leader's expect_tx covers them).
+    uint32_t stage = 0, phase = 0;
+    const uint32_t full0 = smem_u32(&full[0]), empty0 = smem_u32(&empty[0]);
+    const uint32_t sB0 = smem_u32(sB);
+    const int xs = tail_split_count(total_tiles, grid_clusters<kCG>(), C::kHalfTiles);
+    for (int t = cluster_index<kCG>(); t < total_tiles + xs; t += grid_clusters<kCG>()) {
+      const Tile T = decode_unit<kCG, kBN>(t, total_tiles, xs, rank, tab_tile, tab_row, tab_size, tab_crow, G);
+      const int gb = ld_shared_s32(smem_u32(&tab_bidx[T.g]));
+      const int nb = T.n0 + rank * C::kBCols;
+      for (int kb = 0; kb < kbc; ++kb) {
+        mbar_wait_addr(empty0 + 8 * stage, phase ^ 1);
+        const uint32_t fb = full0 + 8 * stage;
+        if (elect_one() && !(dbg & kDbgNoLoad)) {
+          const int cb0 = p.b_kmajor ? kb * BK : nb;
+          const int cb1 = p.b_kmajor ? nb : kb * BK;
+          if (p.l2_b)
+            tma_load_3d_hint<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb, p.l2_b);
+          else
+            tma_load_3d_u32<kCG>(&p.tmap_b, fb, sB0 + stage * C::kStageBytesB, cb0, cb1, gb);
+        }
+        __syncwarp();
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+    }
   } else if (warp == 2) {
     // ========================================================== scale loader
     // Per tile: the S_A over-fetch window (one 1-D bulk copy by lane 0, prefetch.py:50-72) and
