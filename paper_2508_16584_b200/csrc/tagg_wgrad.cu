@@ -212,12 +212,9 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
               mbar_arrive_leader_addr(fb);  // nothing of ours to publish: the TMA bytes count themselves
             }
             tma_load_2d_u32<2>(&p.map_x[lg], fb, a_dst, kr, row0);
-            tma_load_2d_u32<2>(&p.map_dy[lg], fb, b_dst, nr, row0);
-            if (res < BT) {  // dual phase: rows [0, d) above, rows [res - d, res) here
+            if (res < BT)  // dual phase: rows [0, d) above, rows [res - d, res) here
               tma_load_2d_u32<2>(&p.map_x[lg], fb, a_dst + (res - d) * 128u, kr, row0 + res - d);
-              tma_load_2d_u32<2>(&p.map_dy[lg], fb, b_dst + (res - d) * 128u, nr, row0 + res - d);
-            }
-
+            // dY's boxes: warp 2 (a TMA issue holds its warp; one warp issuing every box paced the pipe)
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -229,6 +226,29 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       __syncwarp();
+    } else if (warp == 2) {
+      // ====================================================== dY loads (both CTAs)
+      // The stage's dY boxes (dual phase for a group's last token block; the producer zeroes the
+      // rows past the group end), counted on the same full barrier.
+      uint32_t stage = 0, phase = 0;
+      const uint32_t sB0 = smem_u32(smem + p.off_b);
+      for (int t = cid; t < tiles; t += nclusters) {
+        const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
+        const int nr = (rem % p.NT) * 256 + 128 * rank;
+        const int m = tab_m[g], off = tab_off[g];
+        for (int j = 0; j * BT < m; ++j) {
+          mbar_wait_addr(smem_u32(&empty[stage]), phase ^ 1);
+          if (elect_one()) {
+            const int res = min(BT, m - j * BT), row0 = off + j * BT;
+            const int lg = res == BT ? 7 : 31 - __clz(res), d = 1 << lg;
+            const uint32_t fb = smem_u32(&full[stage]), b_dst = sB0 + stage * kStageB;
+            tma_load_2d_u32<2>(&p.map_dy[lg], fb, b_dst, nr, row0);
+            if (res < BT) tma_load_2d_u32<2>(&p.map_dy[lg], fb, b_dst + (res - d) * 128u, nr, row0 + res - d);
+          }
+          __syncwarp();
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
     } else if (kMx && warp == 3) {
       // ====================================================== E8M0 factor loads (kMx, both CTAs)
       // The stage's factor blocks ride on its full barrier (the leader's expect_tx counts them); a
