@@ -39,6 +39,10 @@ tg.quantize_blocks(torch.randn((2, 256, 384), device=dev))
 xc, xs = tg.quantize_col_blocks(torch.randn((m, 256), device=dev), gs)
 dyc, dys = tg.quantize_col_blocks(torch.randn((m, 128), device=dev), gs)
 tg.wgrad_fp8(xc, xs, dyc, dys, gs)
+# MXFP8 weight gradient: power-of-two quantizer with factor blocks, block-scaled MMA
+xm, _, xf = tg.quantize_col_blocks_mx(torch.randn((m, 256), device=dev), gs)
+dm, _, df = tg.quantize_col_blocks_mx(torch.randn((m, 256), device=dev), gs)
+tg.wgrad_fp8_mx(xm, xf, dm, df, gs)
 # bf16 column quantizer (persistent kernel), plain and gathered
 xb = torch.randn((m, 512), device=dev).to(torch.bfloat16)
 tg.quantize_col_blocks(xb, gs)
