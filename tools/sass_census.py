@@ -2,7 +2,7 @@
 prove the tcgen05 / TMA path (UTCQMMA = tcgen05.mma kind::f8f6f4, LDTM = tcgen05.ld, UTMALDG /
 UTMASTG = TMA tensor load / store, UBLKCP = 1-D bulk copy), the promotion math (FFMA2, FMUL2),
 the bf16 packs, and every local-memory spill with the source line it is attributed to
-(nvdisasm -g; the build uses -lineinfo).  Writes profiles/sass_census_r02.json."""
+(nvdisasm -g; the build uses -lineinfo).  Writes profiles/sass_census_r02b.json."""
 import collections
 import json
 import re
@@ -13,7 +13,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 LIB = ROOT / "paper_2508_16584_b200" / "libtagg.so"
-OPS = ("UTCQMMA", "UTCHMMA", "LDTM", "STTM", "UTMALDG", "UTMASTG", "UBLKCP", "UTCBAR", "FFMA2", "FMUL2", "FFMA", "FMUL",
+OPS = ("UTCQMMA", "UTCHMMA", "UTCCP", "LDTM", "STTM", "UTMALDG", "UTMASTG", "UBLKCP", "UTCBAR", "FFMA2", "FMUL2", "FFMA", "FMUL",
        "FADD", "F2FP.BF16.F32.PACK_AB", "F2FP.SATFINITE.E4M3.F32.PACK_AB_MERGE_C", "HMMA", "LDL", "STL")
 
 
@@ -45,7 +45,7 @@ def main():
                         spills.append(f"{op} @ {line}")
                 dem = subprocess.run(["c++filt"], input=name, capture_output=True, text=True).stdout.strip()
                 out[dem] = {"file": cub.name, "ops": dict(ops), "local_memory": spills}
-    dst = ROOT / "profiles" / "sass_census_r02.json"
+    dst = ROOT / "profiles" / "sass_census_r02b.json"
     dst.write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
     for k, v in out.items():
         if "gemm_kernel" in k or "wgrad" in k:
