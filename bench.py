@@ -724,6 +724,10 @@ def summarize(line, fp8_peak):
     q = ex.get("quantize_dispatch_dsv3")
     if isinstance(q, dict) and "gbs" in q:
         out.append(f"quant+dispatch {f(q['gbs'])} GB/s {f(100 * q['hbm_frac'])}%")
+    cq = ex.get("quantize_col_blocks_dsv3")
+    if isinstance(cq, dict) and isinstance(cq.get("mxfp8"), dict):
+        out.append(f"col quant {f(cq['fp32_scales']['gbs'])} GB/s {f(100 * cq['fp32_scales']['hbm_frac'])}% "
+                   f"(MXFP8 {f(cq['mxfp8']['gbs'])} GB/s {f(100 * cq['mxfp8']['hbm_frac'])}%)")
     ep = ex.get("deepseek_v3_down_ep")
     if isinstance(ep, dict) and "gemm_tflops_aggregate" in ep:
         out.append(f"ep{ep['world']} gemm {f(ep['gemm_tflops_aggregate'])} TF/s e2e {f(ep['e2e_tflops_aggregate_incl_a2a'])}")
@@ -796,6 +800,7 @@ def run_extra(torch, tg, dev, rank, fp8_peak, exact):
         del P
         torch.cuda.empty_cache()
     out["quantize_dispatch_dsv3"] = run_quantize_dispatch(torch, tg, dev)
+    out["quantize_col_blocks_dsv3"] = run_quantize_col_blocks(torch, tg, dev)
     out["wgrad_dsv3_gateup"] = run_wgrad(torch, tg, dev, fp8_peak)
     out["moe_ffn_dsv3_1gpu"] = run_moe_ffn(torch, tg, dev, fp8_peak)
     out["dense_fp8_reference_8192"] = run_dense_reference(torch, tg, dev, fp8_peak)
@@ -844,6 +849,34 @@ def run_wgrad(torch, tg, dev, fp8_peak, iters=5, warmup=2):
     # the headline keys: the per-column recipe (round 1's), then the block one beside it
     res.update({"ms": res["per_column_dy"]["ms"], "tflops": res["per_column_dy"]["tflops"],
                 "fp8_peak_frac": res["per_column_dy"]["fp8_peak_frac"]})
+    return res
+
+
+def run_quantize_col_blocks(torch, tg, dev, rows=262144, cols=7168, groups=256, iters=5, warmup=2):
+    """The weight gradient's column-block quantizer (HBM-bound) on the DeepSeek-V3 backward's
+    grouped activations (262,144 routed rows of bf16 x 7168, 256 experts of 1024 rows): the
+    per-column fp32-scale recipe and the MXFP8 recipe.  Algorithmic bytes = x read + codes
+    written (the scales are 1/32 of the codes)."""
+    peaks = _peaks()[0]
+    gs = torch.full((groups,), rows // groups, dtype=torch.int32, device=dev)
+    x = torch.randn((rows, cols), device=dev, generator=torch.Generator(device=dev).manual_seed(9)).to(torch.bfloat16)
+    nbytes = rows * cols * 3
+    res = {"rows": rows, "cols": cols, "groups": groups, "bytes": nbytes}
+    for label, fn in (("fp32_scales", lambda: tg.quantize_col_blocks(x, gs)),
+                      ("mxfp8", lambda: tg.quantize_col_blocks_mx(x, gs))):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / iters
+        res[label] = {"ms": ms, "gbs": nbytes / ms / 1e6, "hbm_frac": nbytes / ms / 1e6 / float(peaks["hbm_gbs"])}
+    del x
+    torch.cuda.empty_cache()
     return res
 
 

@@ -604,6 +604,16 @@ __device__ __forceinline__ uint32_t e4m3x4_bracket(const float (&v)[4], const fl
   hi_codes = static_cast<uint32_t>(c) | (static_cast<uint32_t>(d) << 16);
   return static_cast<uint32_t>(a) | (static_cast<uint32_t>(b) << 16);
 }
+// Codes of four exact quotients x * (1/s) for a power-of-two s (the MXFP8 recipe).
+__device__ __forceinline__ uint32_t e4m3x4_pow2(const float (&v)[4], const float (&r)[4]) {
+  float l[4];
+  fmul2_rz(l[0], l[1], v[0], v[1], r[0], r[1]);
+  fmul2_rz(l[2], l[3], v[2], v[3], r[2], r[3]);
+  uint16_t a, b;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(a) : "f"(l[1]), "f"(l[0]));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(b) : "f"(l[3]), "f"(l[2]));
+  return static_cast<uint32_t>(a) | (static_cast<uint32_t>(b) << 16);
+}
 // The bracket's undecided case (a few per thousand elements: bf16 data over a bf16 column
 // maximum puts x / s on or next to an e4m3 midpoint that often): the IEEE division decides.
 __device__ __forceinline__ uint32_t e4m3x4_div(const float4 v, const float* s) {
@@ -656,7 +666,7 @@ struct ColChunk {
   }
 };
 
-template <bool kBf16, bool kBlock128, bool kWeighted>
+template <bool kBf16, bool kBlock128, bool kWeighted, bool kPow2 = false>
 __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* __restrict__ x, int64_t ldx, int cols,
                                                                    const int32_t* __restrict__ group_sizes, int G,
                                                                    uint8_t* __restrict__ codes, int64_t ldc,
@@ -843,10 +853,17 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
                                value(cur, j, 4 * h + 3)};
           const float l4[4] = {rlo[4 * h], rlo[4 * h + 1], rlo[4 * h + 2], rlo[4 * h + 3]};
           const float h4[4] = {rhi[4 * h], rhi[4 * h + 1], rhi[4 * h + 2], rhi[4 * h + 3]};
-          w[h] = e4m3x4_bracket(v4, l4, h4, up[h]);
+          if constexpr (kPow2) {
+            // a power-of-two scale: x * (1/s) IS x / s (exact), one product and one conversion
+            w[h] = e4m3x4_pow2(v4, l4);
+            up[h] = w[h];
+          } else {
+            w[h] = e4m3x4_bracket(v4, l4, h4, up[h]);
+          }
           vv[h] = make_float4(v4[0], v4[1], v4[2], v4[3]);
         }
         if (live) *reinterpret_cast<uint2*>(crow + static_cast<int64_t>(16 * j) * ldc) = make_uint2(w[0], w[1]);
+        if constexpr (kPow2) continue;  // nothing is ever undecided
         const bool u = live && (w[0] != up[0] || w[1] != up[1]);
         const uint32_t m = __ballot_sync(0xffffffffu, u);
         if (m) {
@@ -952,7 +969,10 @@ static int quantize_col_blocks_impl(const void* x, int x_dtype, int64_t m_alloc,
     };
     const bool bf16 = x_dtype == TAGG_DTYPE_BF16, w = row_weights != nullptr, b128 = block_cols == 128;
     using namespace wg;
-    if (bf16) {
+    if (pow2 && !b128) {
+      if (bf16) w ? launch(quantize_col_tile_kernel<true, false, true, true>) : launch(quantize_col_tile_kernel<true, false, false, true>);
+      else w ? launch(quantize_col_tile_kernel<false, false, true, true>) : launch(quantize_col_tile_kernel<false, false, false, true>);
+    } else if (bf16) {
       if (b128) w ? launch(quantize_col_tile_kernel<true, true, true>) : launch(quantize_col_tile_kernel<true, true, false>);
       else w ? launch(quantize_col_tile_kernel<true, false, true>) : launch(quantize_col_tile_kernel<true, false, false>);
     } else {
