@@ -106,6 +106,7 @@ struct Params {
   uint64_t l2_c;         // L2 eviction policy of the C stores (0 = no hint)
   float one;             // 1.0f (kExact promotion: an FFMA2 by a 1.0 the compiler cannot see)
   uint32_t stage_tx;     // bytes landing per pipeline stage (both CTAs): A box rows x 128 + B box
+  uint32_t store_warp;   // 1: the scale-loader warp issues the C stores (256-column tiles, one-pass staging)
 };
 
 template <int kCG, int kBN_>
@@ -124,9 +125,9 @@ struct Cfg {
 // Diagnostics trace: stamps of the first kTraceLen k-block iterations of CTAs 0 and 1.
 // Compiled in only with -DTAGG_TRACE (libtagg_trace.so, `make trace`; tools/trace.py).
 constexpr int kTraceLen = 1024;
-constexpr int kTraceEvents = 10;
+constexpr int kTraceEvents = 12;
 enum TraceEv { kEvMmaTempty = 0, kEvMmaFull, kEvMmaIssued, kEvProdEmpty, kEvPromoFull, kEvPromoFreed, kEvPromoDone,
-               kEvPromo2Full, kEvEpiStart, kEvEpiEnd };
+               kEvPromo2Full, kEvEpiStart, kEvEpiEnd, kEvEpiBar1, kEvEpiStores };
 __device__ __forceinline__ void trace_stamp(unsigned long long* tr, int ev, uint32_t i) {
 #ifdef TAGG_TRACE
   if (tr != nullptr && blockIdx.x < 2 && i < static_cast<uint32_t>(kTraceLen))
@@ -332,7 +333,9 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
   uint64_t* tempty = tfull + C::kNumAcc;
   uint64_t* safull = tempty + C::kNumAcc;
   uint64_t* saempty = safull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(saempty + 2);
+  uint64_t* cfull = saempty + 2;   // C staging half h written (its 4 promotion warps)
+  uint64_t* cempty = cfull + 2;    // C staging reusable (the store warp, after its stores' reads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
 
   // ------------------------------------------------------------ prologue
   if (warp == 0 && lane == 0) {
@@ -349,6 +352,8 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     for (int i = 0; i < 2; ++i) {
       mbar_init(&safull[i], 1 + 32);  // S_A bulk copy (expect_tx) + 32 scale-loader lanes' S_B cp.async
       mbar_init(&saempty[i], kNumPromoWarps);
+      mbar_init(&cfull[i], kNumPromoWarps / 2);
+      mbar_init(&cempty[i], 1);
     }
     fence_mbar_init();
   }
@@ -525,6 +530,74 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t nslots = p.sa_slots;
     const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
+    // With p.store_warp (256-column tiles, one-pass staging) this warp also issues the C stores:
+    // a TMA issue holds its warp for ~500 clk per tile (traced), which, in the promotion warp
+    // that used to issue them, delayed that warp's next drain and with it the whole MMA chain.
+    // The promotion warps hand over through cfull[h] (their half written) and get the staging
+    // back through cempty[h] (the stores have read it).  Tile t's stores are issued after tile
+    // t + 1's scale window is requested, so the window never waits behind a store.
+    uint32_t cph = 0;
+    bool prev_grid_done = !p.pdl_overlap;  // default mode waited in the prologue
+    const uint32_t cfull0 = smem_u32(&cfull[0]), cempty0 = smem_u32(&cempty[0]);
+    auto store_tile = [&](const Tile& T, int t) {
+      mbar_wait_addr(cfull0, cph);
+      mbar_wait_addr(cfull0 + 8, cph);
+      cph ^= 1;
+      if (lane == 0 && T.valid > 0) {
+        if (!prev_grid_done) {
+          griddep_wait();  // WAW on C / tile_map with the previous grid: store only after it completed
+          prev_grid_done = true;
+        }
+        const int lg = 31 - __clz(T.valid);
+        const int d = 1 << lg;
+        if (C::kHalfTiles && T.half) {
+          // half tile: 4 chunks of 64 rows x 64 columns, this CTA's <= 64 rows (64-row plan)
+          constexpr uint32_t kHalfChunk = kChunkBytesC / 2;
+          for (int ch = 0; ch < 4; ++ch) {
+            const int col = T.n0 + 64 * ch;
+            if (col >= p.N) break;
+            const uint8_t* chunk = sC + ch * kHalfChunk;
+            store_c(p, lg, chunk, col, T.crow0);
+            if (T.valid != BM / 2) store_c(p, lg, chunk + static_cast<uint32_t>(T.valid - d) * 128u, col, T.crow0 + T.valid - d);
+          }
+        } else {
+          for (int ch = 0; ch < 4; ++ch) {
+            const int col = T.n0 + 64 * ch;
+            if (col >= p.N) break;
+            const uint8_t* chunk = sC + ch * kChunkBytesC;
+            store_c(p, lg, chunk, col, T.crow0);  // phase a
+            if (T.valid != BM)                     // phase b (both, even if they coincide)
+              store_c(p, lg, chunk + static_cast<uint32_t>(T.valid - d) * 128u, col, T.crow0 + T.valid - d);
+          }
+        }
+        bulk_commit();
+        if (p.tile_map) {
+          for (int sub = 0; sub < 2; ++sub) {
+            const int n0 = T.n0 + 128 * sub;
+            if (n0 >= p.N) continue;
+            int32_t* rec = p.tile_map + ((static_cast<int64_t>(t) * kCG + rank) * 2 + sub) * TAGG_TILE_MAP_FIELDS;
+            rec[0] = T.g;
+            rec[1] = T.mt;
+            rec[2] = n0;
+            rec[3] = T.row0;
+            rec[4] = T.valid;
+            rec[5] = d;
+            rec[6] = T.crow0;
+            rec[7] = T.valid - d;
+            rec[8] = T.crow0 + T.valid - d;
+          }
+        }
+      }
+      if (lane == 0) {
+        bulk_wait_read0();  // the stores have read the staging
+        mbar_arrive_addr(cempty0);
+        mbar_arrive_addr(cempty0 + 8);
+      }
+      __syncwarp();
+    };
+    const bool stores = p.store_warp != 0;
+    Tile Tprev;
+    int tprev = -1;
     const int xs = tail_split_count(total_tiles, grid_clusters<kCG>(), C::kHalfTiles);
     for (int t = cluster_index<kCG>(); t < total_tiles + xs; t += grid_clusters<kCG>()) {
       const Tile T = decode_unit<kCG, kBN>(t, total_tiles, xs, rank, tab_tile, tab_row, tab_size, tab_crow, G);
@@ -532,7 +605,14 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
       mbar_wait_addr(sempty0 + 8 * sab, saph ^ 1);
       load_scale_window(p, T, gb, sab, sfull0, sSA0, sSB0, sSA, kbc, rb, lane);
       if (++sab == nslots) { sab = 0; saph ^= 1; }
+      if (stores) {
+        if (tprev >= 0) store_tile(Tprev, tprev);
+        Tprev = T;
+        tprev = t;
+      }
     }
+    if (stores && tprev >= 0) store_tile(Tprev, tprev);
+    if (stores && lane == 0) bulk_wait0();
     __syncwarp();
   } else if (warp == 1) {
     // ========================================================== MMA issuer (leader CTA)
@@ -610,8 +690,10 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
     const uint32_t sfull0 = opaque_u32(smem_u32(&safull[0])), sempty0 = opaque_u32(smem_u32(&saempty[0]));
     const uint32_t sSA0 = opaque_u32(smem_u32(sSA)), sSB0 = opaque_u32(smem_u32(sSB));
     const float one = p.one;  // 1.0f from the launch parameters: ptxas cannot fold it
-    uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0, tiles_done = 0;
+    uint32_t acc_i = 0, accph = 0, sab = 0, saph = 0, kiter = 0, tiles_done = 0, cep = 0;
     bool prev_grid_done = !p.pdl_overlap;  // default mode waited in the prologue
+    const bool store_warp = p.store_warp != 0;
+    const uint32_t cfull_h = opaque_u32(smem_u32(&cfull[half])), cempty_h = opaque_u32(smem_u32(&cempty[half]));
 #ifdef TAGG_TRACE
     const bool tr_a = p.trace != nullptr && pw == 0 && lane == 0;
     const bool tr_b = p.trace != nullptr && pw == 4 && lane == 0;
@@ -673,8 +755,12 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         const int lg = T.valid > 0 ? 31 - __clz(T.valid) : 0;
         const int d = 1 << lg;
         constexpr uint32_t kHalfChunk = kChunkBytesC / 2;
-        if (ptid == 0) bulk_wait_read0();
-        named_bar_sync(1, 32 * kNumPromoWarps);
+        if (store_warp) {
+          mbar_wait_addr(cempty_h, cep ^ 1);  // the store warp has read the previous tile's staging
+        } else {
+          if (ptid == 0) bulk_wait_read0();
+          named_bar_sync(1, 32 * kNumPromoWarps);
+        }
         {
           const uint32_t base = smem_u32(sC) + static_cast<uint32_t>(hcol >> 6) * kHalfChunk + hrow * 128u;
 #pragma unroll
@@ -687,6 +773,13 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
             st_shared_v4(base + c16 * 16u, w0, w1, w2, w3);
           }
           fence_proxy_async_smem();
+        }
+        if (store_warp) {
+          // hand the staging to the store warp (warp 2), which also writes the tile-map records
+          __syncwarp();
+          if (lane == 0) mbar_arrive_addr(cfull_h);
+          cep ^= 1;
+          continue;
         }
         named_bar_sync(1, 32 * kNumPromoWarps);
         if (ptid == 0 && T.valid > 0 && !prev_grid_done) {
@@ -868,8 +961,13 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
         // issuing thread, so each half's leader waits for its own earlier stores; the half-tile
         // path stages in [0, 32 KB) only, i.e. in half 0's chunks, and stores from thread 0.
         const int hl = 128 * half;  // ptid of this half's leader
-        if (ptid == hl) bulk_wait_read0();
-        named_bar_sync(2 + half, 128);
+        if (store_warp) {
+          mbar_wait_addr(cempty_h, cep ^ 1);  // the store warp has read the previous tile's staging
+        } else {
+          if (ptid == hl) bulk_wait_read0();
+          named_bar_sync(2 + half, 128);
+        }
+        if (tr_a) trace_stamp(p.trace, kEvEpiBar1, tiles_done);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int chunk = 2 * half + (j >> 3);
@@ -883,11 +981,21 @@ __global__ void __launch_bounds__(kThreads, 1) tagg_gemm_kernel(const __grid_con
                        w3);
         }
         fence_proxy_async_smem();
+        if (store_warp) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_addr(cfull_h);
+          cep ^= 1;
+          if (tr_a) trace_stamp(p.trace, kEvEpiStores, tiles_done);
+          if (tr_a) trace_stamp(p.trace, kEvEpiEnd, tiles_done);
+          ++tiles_done;
+          continue;
+        }
         named_bar_sync(2 + half, 128);
         if (ptid == hl && T.valid > 0 && !prev_grid_done) {
           griddep_wait();  // WAW on C / tile_map with the previous grid: store only after it completed
           prev_grid_done = true;
         }
+        if (tr_a) trace_stamp(p.trace, kEvEpiStores, tiles_done);
         if (ptid == hl && T.valid > 0 && T.n0 + 128 * half < p.N) {
           for (int ch = 2 * half; ch < 2 * half + 2; ++ch) {
             const int col = T.n0 + 64 * ch;
@@ -1128,7 +1236,7 @@ static uint32_t smem_layout(Params& p, uint32_t stages, int G, int rb, int num_a
   p.off_tab = p.off_sb + sa_slots * kSbBufBytes;
   const uint32_t tab_bytes = align_up(4u * static_cast<uint32_t>(2 * (G + 1) + 3 * G), 16);
   p.off_bar = p.off_tab + tab_bytes;
-  const uint32_t bar_bytes = (2 * stages + 2 * num_acc + 4) * 8 + 16;
+  const uint32_t bar_bytes = (2 * stages + 2 * num_acc + 8) * 8 + 16;
   return p.off_bar + bar_bytes + 1024;
 }
 
@@ -1350,6 +1458,9 @@ extern "C" int tagg_grouped_gemm_fp8_ex(const void* a, int64_t lda, const float*
   }
   if (p.epi_passes != 1) stages = fit(kCStagingBytes, slots);
   const uint32_t staging = p.epi_passes == 1 ? 2 * kCStagingBytes : kCStagingBytes;
+  // 256-column pair tiles with the one-pass staging: the scale-loader warp issues the C stores
+  static const int env_sw = [] { const char* e = std::getenv("TAGG_STORE_WARP"); return e ? std::atoi(e) : 1; }();
+  p.store_warp = (cg == 2 && bn == 256 && p.epi_passes == 1 && env_sw) ? 1u : 0u;
   if (stages >= 2) smem_bytes = smem_layout(p, stages, G, rb, num_acc, stage_bytes_b, staging, slots);
   if (stages < 2) return TAGG_ERR_UNSUPPORTED;
 

@@ -17,9 +17,9 @@ for name, (res, args) in _lib.SIGNATURES.items():
     fn.restype, fn.argtypes = res, args
 
 EV = ["mma_tempty", "mma_full", "mma_issued", "prod_empty", "promo_full", "promo_freed", "promo_done", "promo2_full",
-      "epi_start", "epi_end"]
+      "epi_start", "epi_end", "epi_bar1", "epi_stores"]
 dev = torch.device("cuda", 0)
-buf = torch.zeros((2, 10, 1024), dtype=torch.int64, device=dev)
+buf = torch.zeros((2, len(EV), 1024), dtype=torch.int64, device=dev)
 
 
 def run(P, flags, G):
@@ -53,6 +53,10 @@ def report(tr, lo, hi, label):
     if nt > 1:
         dur = ee[:nt] - es[:nt]
         print(f"  epilogue per tile (clk): median {np.median(dur):.0f} over {nt} tiles")
+        b1, st = t[EV.index("epi_bar1")][:nt], t[EV.index("epi_stores")][:nt]
+        if (b1 > 0).all():
+            print(f"    start->barrier {np.median(b1 - es[:nt]):.0f} | barrier->staged {np.median(st - b1):.0f} | "
+                  f"store issue {np.median(ee[:nt] - st):.0f}")
     t1 = tr[1].astype(np.float64)
     v = t1[EV.index("promo_full"), lo:hi] - t1[EV.index("promo_full"), lo - 1:hi - 1]
     print(f"  {'CTA1 promo full period':38s} {np.median(v):8.0f}")
