@@ -639,13 +639,14 @@ template <bool kBf16>
 struct ColChunk {
   using Raw = typename std::conditional<kBf16, uint4, float4[2]>::type;
   Raw raw[8];
-  __device__ __forceinline__ void load(const void* x, int64_t ldx, const int64_t (&src)[8], int c) {
+  // rows[j]: row j's first element (x + src_j * ldx), formed once per CTA
+  __device__ __forceinline__ void load(const char* const (&rows)[8], int c) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       if constexpr (kBf16) {
-        raw[j] = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + src[j] * ldx + c));
+        raw[j] = __ldcs(reinterpret_cast<const uint4*>(rows[j] + 2 * static_cast<int64_t>(c)));
       } else {
-        const float4* f = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + src[j] * ldx + c);
+        const float4* f = reinterpret_cast<const float4*>(rows[j] + 4 * static_cast<int64_t>(c));
         raw[j][0] = __ldcs(f);
         raw[j][1] = __ldcs(f + 1);
       }
@@ -726,14 +727,21 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
   // Rows past the block read a clamped live row: all 8 loads go out without a branch, and a
   // duplicate of a live row leaves every column maximum unchanged (such rows are never stored).
   // Columns past `cols` read a clamped live column the same way (their scales are not written).
-  int64_t src[8];
+  const char* xrow[8];
   float wr[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int64_t rg = row0 + min(rl + 16 * j, rows - 1);
-    src[j] = index ? static_cast<int64_t>(__ldg(index + rg)) : rg;
+    const int64_t src = index ? static_cast<int64_t>(__ldg(index + rg)) : rg;
+    xrow[j] = reinterpret_cast<const char*>(x) + src * ldx * (kBf16 ? 2 : 4);
     wr[j] = kWeighted ? __ldg(row_weights + rg) : 1.0f;
   }
+  // this thread's live rows (bit j: row rl + 16 j < rows) and its first code row
+  uint32_t live_rows = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) live_rows |= (rl + 16 * j < rows ? 1u : 0u) << j;
+  uint8_t* const code_row = codes + (row0 + rl) * ldc;
+  const int64_t code_step = 16 * ldc;
   auto value = [&](const ColChunk<kBf16>& ch, int j, int k) -> float {
     const float f = ch.get(j, k);
     return kWeighted ? __fmul_rn(wr[j], f) : f;  // weighted rows are fl(w * x), as gathered
@@ -745,20 +753,30 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
   // (measured: without the prefetch, 3 CTAs per SM run 3-5% slower)
   constexpr bool kPrefetch = kBf16;
   ColChunk<kBf16> cur;
-  if (kPrefetch) cur.load(x, ldx, src, min(cg * 8, cols - 8));
+  if (kPrefetch) cur.load(xrow, min(cg * 8, cols - 8));
   for (int cb = 0; cb < nchunks; ++cb) {
     const int c0 = cb * 128 + cg * 8;
     ColChunk<kBf16> nxt;
-    if (!kPrefetch) cur.load(x, ldx, src, min(c0, cols - 8));
-    if (kPrefetch && cb + 1 < nchunks) nxt.load(x, ldx, src, min(c0 + 128, cols - 8));
+    if (!kPrefetch) cur.load(xrow, min(c0, cols - 8));
+    if (kPrefetch && cb + 1 < nchunks) nxt.load(xrow, min(c0 + 128, cols - 8));
     const int buf = cb & 1;
     uint32_t amax[8];  // |x| bit patterns: integer order = float order for non-negative floats
     if constexpr (kBf16 && !kWeighted) {
-      uint32_t pw[4] = {0u, 0u, 0u, 0u};  // packed pairs
+      // |x| maxima of packed pairs without masking each word: a signed 16-bit max finds the
+      // largest non-negative pattern, an unsigned one the largest negative (sign-magnitude: the
+      // unsigned order of negative patterns is their |x| order); with the sign bits cleared, the
+      // larger of the two is max |x| (and NaN / inf still sort above every finite value)
+      uint32_t ps[4] = {0x80008000u, 0x80008000u, 0x80008000u, 0x80008000u}, pu[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
       for (int j = 0; j < 8; ++j)
 #pragma unroll
-        for (int h = 0; h < 4; ++h) pw[h] = __vmaxu2(pw[h], cur.word(j, h) & 0x7FFF7FFFu);
+        for (int h = 0; h < 4; ++h) {
+          ps[h] = __vmaxs2(ps[h], cur.word(j, h));
+          pu[h] = __vmaxu2(pu[h], cur.word(j, h));
+        }
+      uint32_t pw[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) pw[h] = __vmaxu2(ps[h] & 0x7FFF7FFFu, pu[h] & 0x7FFF7FFFu);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         amax[2 * h] = pw[h] << 16;
@@ -824,7 +842,8 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
         rhi[0] = e.x; rhi[1] = e.y; rhi[2] = e.z; rhi[3] = e.w; rhi[4] = f.x; rhi[5] = f.y; rhi[6] = f.z; rhi[7] = f.w;
       }
       const uint32_t lt = (1u << lane) - 1u;
-      uint8_t* const crow = codes + (row0 + rl) * ldc + c0;  // this thread's first row
+      uint8_t* crow = code_row + c0;  // this thread's row rl + 16 j, advanced by code_step
+      const uint32_t live_mask = c_ok ? live_rows : 0u;
       int qn = 0;  // warp-uniform
       auto drain_queue = [&]() {
         __syncwarp();  // the rows' bracket codes are stored before any patch
@@ -844,7 +863,7 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int r = rl + 16 * j;
-        const bool live = c_ok && r < rows;
+        const bool live = (live_mask >> j) & 1u;
         uint32_t w[2], up[2];
         float4 vv[2];
 #pragma unroll
@@ -862,7 +881,8 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
           }
           vv[h] = make_float4(v4[0], v4[1], v4[2], v4[3]);
         }
-        if (live) *reinterpret_cast<uint2*>(crow + static_cast<int64_t>(16 * j) * ldc) = make_uint2(w[0], w[1]);
+        if (live) *reinterpret_cast<uint2*>(crow) = make_uint2(w[0], w[1]);
+        crow += code_step;
         if constexpr (kPow2) continue;  // nothing is ever undecided
         const bool u = live && (w[0] != up[0] || w[1] != up[1]);
         const uint32_t m = __ballot_sync(0xffffffffu, u);
