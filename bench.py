@@ -352,18 +352,23 @@ def run_problem_set(torch, tg, prob, iters, warmup, flush=None, exact=False):
             tg.padded_grouped_gemm_fp8(prob.a, prob.sa, prob.b, prob.sb, gs, ws, b_layout=prob.b_layout, out=outs,
                                        unpad=unpad, exact_promotion=exact)
 
-    res = {}
-    for name, fn in (("adaptive", adaptive), ("padded", padded), ("padded_no_unpad", lambda: padded(False))):
-        for _ in range(warmup):
-            fn()
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for _ in range(iters):
-            fn()
-        e.record()
-        torch.cuda.synchronize()
-        res[name] = s.elapsed_time(e) / iters
+    # three rounds in rotating order, median per arm: the first block after an idle gap runs at
+    # a higher clock (power state), so a fixed order would favour whichever arm goes first
+    arms = [("adaptive", adaptive), ("padded", padded), ("padded_no_unpad", lambda: padded(False))]
+    times = {name: [] for name, _ in arms}
+    for rnd in range(3):
+        for name, fn in arms[rnd:] + arms[:rnd]:
+            for _ in range(warmup):
+                fn()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(iters):
+                fn()
+            e.record()
+            torch.cuda.synchronize()
+            times[name].append(s.elapsed_time(e) / iters)
+    res = {name: sorted(v)[1] for name, v in times.items()}
     flops = sum(prob.flops)
     return {k: flops / (v * 1e-3) / 1e12 for k, v in res.items()}, res, ws.nbytes()
 
