@@ -158,29 +158,15 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     setmaxnreg_dec<72>();
     if (warp == 0) {
       // ====================================================== producer (both CTAs)
-      uint32_t stage = 0, phase = 0, sring = 0, sph = 0, piter = 0;
+      uint32_t stage = 0, phase = 0, piter = 0;
       const uint32_t sA0 = smem_u32(smem + p.off_a), sB0 = smem_u32(smem + p.off_b);
-      const uint32_t sS0 = smem_u32(smem + p.off_s);
       for (int t = cid; t < tiles; t += nclusters) {
         const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
         const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
-        const int kr = k0 + 128 * rank, nr = n0 + 128 * rank;  // this CTA's K rows, B columns
-        const int m = tab_m[g], off = tab_off[g], tb0 = tab_tb[g];
+        const int kr = k0 + 128 * rank;  // this CTA's K rows
+        const int m = tab_m[g], off = tab_off[g];
         for (int j = 0; j * BT < m; ++j) {
-          // scales of this token block: sx[tb][kr..+128), sdy[tb][n0..+256) (kMx: E8M0 factor blocks
-          // loaded with the operands below instead)
-          if (!kMx) mbar_wait_addr(smem_u32(&sempty[sring]), sph ^ 1);
-          if (!kMx && lane == 0) {
-            const uint32_t dst = sS0 + sring * kScaleSlot;
-            const int64_t tb = tb0 + j;
-            const uint32_t nsx = kr < p.K ? 512u : 0u;
-            const uint32_t nsdy = n0 + 256 <= p.N ? 1024u : 512u;
-            mbar_arrive_expect_tx_addr(smem_u32(&sfull[sring]), nsx + nsdy);
-            if (nsx) bulk_load_1d_addr(dst, p.sx + tb * p.K + kr, nsx, smem_u32(&sfull[sring]));
-            bulk_load_1d_addr(dst + 512, p.sdy + tb * p.N + n0, nsdy, smem_u32(&sfull[sring]));
-          }
-          if (!kMx && ++sring == kScaleRing) { sring = 0; sph ^= 1; }
-          // operands
+          // X boxes (the per-column scales are warp 3's, dY's warp 2's)
           mbar_wait_addr(smem_u32(&empty[stage]), phase ^ 1);
           if (lane == 0) wg_stamp(p.trace, kWgProdEmpty, piter);
           ++piter;
@@ -247,6 +233,33 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    } else if (!kMx && warp == 3) {
+      // ====================================================== scale loads (both CTAs)
+      // sx[tb][kr..+128) and sdy[tb][n0..+256) of each token block into the scale ring, on a warp
+      // of their own: a bulk-copy issue holds its warp, and on the operand producer's warp the
+      // two per block paced the pipeline.
+      uint32_t sring = 0, sph = 0;
+      const uint32_t sS0 = smem_u32(smem + p.off_s);
+      for (int t = cid; t < tiles; t += nclusters) {
+        const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
+        const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
+        const int kr = k0 + 128 * rank;
+        const int m = tab_m[g], tb0 = tab_tb[g];
+        for (int j = 0; j * BT < m; ++j) {
+          mbar_wait_addr(smem_u32(&sempty[sring]), sph ^ 1);
+          if (lane == 0) {
+            const uint32_t dst = sS0 + sring * kScaleSlot;
+            const int64_t tb = tb0 + j;
+            const uint32_t nsx = kr < p.K ? 512u : 0u;
+            const uint32_t nsdy = n0 + 256 <= p.N ? 1024u : 512u;
+            mbar_arrive_expect_tx_addr(smem_u32(&sfull[sring]), nsx + nsdy);
+            if (nsx) bulk_load_1d_addr(dst, p.sx + tb * p.K + kr, nsx, smem_u32(&sfull[sring]));
+            bulk_load_1d_addr(dst + 512, p.sdy + tb * p.N + n0, nsdy, smem_u32(&sfull[sring]));
+          }
+          __syncwarp();
+          if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
         }
       }
     } else if (kMx && warp == 3) {
@@ -404,7 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
         }
       } else
       for (int j = 0; j * BT < m; ++j) {
+#ifndef TAGG_WG_EXP_NOSFULL
         mbar_wait_addr(sfull0 + 8 * sring, sph);
+#endif
         if (tr) wg_stamp(p.trace, kWgPromoSfull, kiter);
         const uint32_t slot = sS0 + sring * kScaleSlot;
         const float sxk = ld_shared_f32(slot + 4u * r);
@@ -425,6 +440,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
             if (lane == 0) mbar_arrive_leader_addr(tempty0 + 8 * acc_i);
             if (tr) wg_stamp(p.trace, kWgPromoFreed, kiter);
           }
+#ifdef TAGG_WG_EXP_NOMATH
+          if (__uint_as_float(v[5]) == 1.2345f) acc[c2] += __uint_as_float(v[7]);
+          continue;
+#endif
           if constexpr (kDyBlock) {
             // acc = fl(acc + inner * s), s = fl(sx * sdy): one FFMA2 per pair, as in the forward
 #pragma unroll

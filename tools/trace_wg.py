@@ -11,7 +11,8 @@ import paper_2508_16584_b200 as tg  # noqa: E402
 from bench import deepseek_gateup_sizes  # noqa: E402
 from paper_2508_16584_b200 import _lib  # noqa: E402
 
-L = ctypes.CDLL(str(_lib.PKG / "libtagg_trace.so"))
+import os
+L = ctypes.CDLL(os.environ.get("TAGG_TRACE_LIB", str(_lib.PKG / "libtagg_trace.so")))
 for name, (res, args) in _lib.SIGNATURES.items():
     if hasattr(L, name):
         fn = getattr(L, name)
