@@ -40,6 +40,10 @@ constexpr int kNumAcc = 2;              // TMEM buffers of 256 columns
 #define WG_STAGES 4
 #endif
 constexpr int kStages = WG_STAGES;
+// dW staging: 64 KB in one pass (the promotion recipes: their epilogue is on the promotion chain)
+// or 32 KB in two (MXFP8: the epilogue runs after the accumulator is released, and the two-pass
+// form measured 7% faster there -- ABBA, tools/wg_ab.py)
+__host__ __device__ constexpr int epi_passes(bool mx) { return mx ? 2 : 1; }
 constexpr int kScaleRing = 8;           // k-block scale slots: sx 128 + sdy 256 floats
 constexpr uint32_t kStageA = BT * 128;  // 128 token rows x this CTA's 128 K columns
 constexpr uint32_t kStageB = BT * 128;  // 128 token rows x this CTA's 128 N columns
@@ -477,31 +481,40 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
         if (++acc_i == kNumAcc) { acc_i = 0; accph ^= 1; }
       }
       if (tr) wg_stamp(p.trace, kWgEpiStart, tiles_done);
-      // epilogue: one pass, 4 chunks of 64 columns x 128 rows (64 KB).  The two column halves
-      // are independent: warps of half h write chunks 2h, 2h+1 (their 128 columns), sync only
-      // among themselves (named barrier 2 + h) and their first thread stores them (a TMA
-      // store's smem reads are tracked per issuing thread, so each leader waits for its own).
+      // epilogue: 4 chunks of 64 columns x 128 rows (64 KB) in epi_passes(kMx) passes over 64 or 32 KB
+      // of staging.  The two column halves are independent: warps of half h write chunks 2h,
+      // 2h+1 (their 128 columns), sync only among themselves (named barrier 2 + h) and their first
+      // thread stores them (a TMA store's smem reads are tracked per issuing thread, so each leader
+      // waits for its own before the slot is rewritten).
       {
+        constexpr int kEpiPasses = epi_passes(kMx);
+        constexpr int kCpp = 2 / kEpiPasses;  // chunks per half per pass
         const int hl = 128 * half;
-        if (ptid == hl) bulk_wait_read0();
-        named_bar_sync(2 + half, 128);
         const uint32_t base = smem_u32(smem + p.off_c) + static_cast<uint32_t>(r) * 128u;
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const uint32_t chunk = 2 * half + (jj >> 3);
-          const uint32_t w0 = pack_bf16x2(acc[8 * jj + 0], acc[8 * jj + 1]);
-          const uint32_t w1 = pack_bf16x2(acc[8 * jj + 2], acc[8 * jj + 3]);
-          const uint32_t w2 = pack_bf16x2(acc[8 * jj + 4], acc[8 * jj + 5]);
-          const uint32_t w3 = pack_bf16x2(acc[8 * jj + 6], acc[8 * jj + 7]);
-          st_shared_v4(base + chunk * kChunkC + static_cast<uint32_t>(((jj & 7) ^ (r & 7)) * 16), w0, w1, w2, w3);
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(2 + half, 128);
-        if (ptid == hl && kr < p.K) {
-          const int row = g * p.K + kr;
-          for (int c = 2 * half; c < 2 * half + 2; ++c)
-            if (n0 + 64 * c < p.N) tma_store_2d(&p.map_dw, smem + p.off_c + c * kChunkC, n0 + 64 * c, row);
-          bulk_commit();
+        for (int ps = 0; ps < kEpiPasses; ++ps) {
+          if (ptid == hl) bulk_wait_read0();
+          named_bar_sync(2 + half, 128);
+#pragma unroll
+          for (int jj = 8 * kCpp * ps; jj < 8 * kCpp * (ps + 1); ++jj) {
+            const uint32_t slot = kCpp * half + ((jj >> 3) - kCpp * ps);
+            const uint32_t w0 = pack_bf16x2(acc[8 * jj + 0], acc[8 * jj + 1]);
+            const uint32_t w1 = pack_bf16x2(acc[8 * jj + 2], acc[8 * jj + 3]);
+            const uint32_t w2 = pack_bf16x2(acc[8 * jj + 4], acc[8 * jj + 5]);
+            const uint32_t w3 = pack_bf16x2(acc[8 * jj + 6], acc[8 * jj + 7]);
+            st_shared_v4(base + slot * kChunkC + static_cast<uint32_t>(((jj & 7) ^ (r & 7)) * 16), w0, w1, w2, w3);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(2 + half, 128);
+          if (ptid == hl && kr < p.K) {
+            const int row = g * p.K + kr;
+            for (int cc = 0; cc < kCpp; ++cc) {
+              const int c = 2 * half + kCpp * ps + cc;  // 64-column chunk of the tile
+              if (n0 + 64 * c < p.N)
+                tma_store_2d(&p.map_dw, smem + p.off_c + (kCpp * half + cc) * kChunkC, n0 + 64 * c, row);
+            }
+            bulk_commit();
+          }
         }
       }
       if (tr) wg_stamp(p.trace, kWgEpiEnd, tiles_done);
@@ -1111,7 +1124,7 @@ static int wgrad_launch(const void* x, const float* sx, const void* dy, const fl
   p.off_a = 0;
   p.off_b = p.off_a + kStages * kStageA;
   p.off_c = p.off_b + kStages * kStageB;
-  p.off_s = p.off_c + 4 * kChunkC;
+  p.off_s = p.off_c + (4 / epi_passes(mx)) * kChunkC;
   p.off_sf = p.off_s + kScaleRing * kScaleSlot;
   p.off_tab = p.off_sf + kStages * kSfStage;
   const uint32_t tab = static_cast<uint32_t>(((3 * G * 4) + 15) & ~15);

@@ -52,3 +52,17 @@ for i in range(40):
 for i in range(8):
     print(f"  tile {i}: acc full seen {E['promo_full'][i] - t0:9.0f}  freed {E['promo_freed'][i] - t0:9.0f}  "
           f"epi {E['epi_start'][i] - t0:9.0f} -> {E['epi_end'][i] - t0:9.0f}")
+lo, hi = 40, 600
+
+
+def d(a, b, sh=0):
+    return E[a][lo:hi] - E[b][lo - sh:hi - sh]
+
+
+print(f"--- medians over k-blocks [{lo},{hi}) of CTA 0 (clk): median / p10 / p90")
+for name, v in {"mma issue period": d("mma_issued", "mma_issued", 1),
+                "mma full seen -> issued": d("mma_issued", "mma_full"),
+                "prod empty period": d("prod_empty", "prod_empty", 1),
+                "prod empty -> mma full (load latency)": d("mma_full", "prod_empty"),
+                "mma issued -> next full seen": d("mma_full", "mma_issued", 1)}.items():
+    print(f"  {name:40s} {np.median(v):8.0f} {np.percentile(v, 10):8.0f} {np.percentile(v, 90):8.0f}")
