@@ -150,6 +150,43 @@ def test_col_block_gather_equals_quantizing_the_gathered_copy(dtype):
     assert torch.equal(plain_c, want_pc) and torch.equal(plain_s[:tb], want_ps[:tb])
 
 
+_SPECIAL_BITS = {  # bit patterns: (bf16 as int16, f32 as int32)
+    "+inf": (0x7F80, 0x7F800000), "-inf": (-0x0080, -0x00800000),
+    "+nan": (0x7FC0, 0x7FC00000), "-nan": (-0x0040, -0x00400000),
+}
+
+
+@pytest.mark.parametrize("special", sorted(_SPECIAL_BITS))
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("path", ["per_column", "block128", "gather", "mxfp8"])
+def test_quantize_col_blocks_flags_non_finite(special, dtype, path):
+    """Every column-block quantizer path flags an inf / NaN of either sign in a live row (the
+    reference raises InvalidInput, fp8.py:54-80); the same matrix with the value made finite
+    passes.  A negative NaN is the case the packed-bf16 |x| maximum reaches through its unsigned
+    half, a positive one through its signed half."""
+    torch.manual_seed(9)
+    sizes = (130, 0, 77)
+    m, c = sum(sizes), 256
+    x = torch.randn((m, c), device=DEV).to(dtype)
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    idx = torch.arange(m, device=DEV, dtype=torch.int32).flip(0)
+
+    def run(t):
+        if path == "mxfp8":
+            return tg.quantize_col_blocks_mx(t, gs, check=True)
+        if path == "gather":
+            return tg.quantize_col_blocks(t, gs, check=True, index=idx)
+        return tg.quantize_col_blocks(t, gs, check=True, block_cols=128 if path == "block128" else 1)
+
+    run(x)
+    bits = _SPECIAL_BITS[special][0 if dtype == torch.bfloat16 else 1]
+    for r, col in ((0, 0), (129, 255), (m - 1, 131)):
+        y = x.clone()
+        y.view(torch.int16 if dtype == torch.bfloat16 else torch.int32)[r, col] = bits
+        with pytest.raises(tg.InvalidInput):
+            run(y)
+
+
 def _sf_blocks(scales):
     """The E8M0 factor blocks tagg_quantize_col_blocks_mx lays out: per (token block, 128
     columns) byte 16 l + 4 c + j = the exponent byte of column 32 c + l's scale (j = 0..3)."""
