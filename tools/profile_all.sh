@@ -15,4 +15,10 @@ $FULL -k regex:tagg_gemm -s 1 -c 1 -o gpurun_out/prof_ds_${TAG} -f python tools/
 $FULL -k regex:tagg_gemm -s 1 -c 1 -o gpurun_out/prof_dsdown_${TAG} -f python tools/prof_one.py ds_down 0 2 >> gpurun_out/ncu_full_${TAG}.log 2>&1
 $FULL -k regex:quantize_dispatch -s 1 -c 1 -o gpurun_out/prof_qd_${TAG} -f python tools/qd_bench.py >> gpurun_out/ncu_full_${TAG}.log 2>&1
 $FULL -k regex:wgrad_kernel -s 1 -c 1 -o gpurun_out/prof_wg_${TAG} -f python tools/wg_bench.py >> gpurun_out/ncu_full_${TAG}.log 2>&1
+# wg_bench launches per recipe: 2 warm-up + 5 timed each (per-column, 128x128 dY, MXFP8)
+$FULL -k regex:wgrad_kernel -s 8 -c 1 -o gpurun_out/prof_wgb_${TAG} -f python tools/wg_bench.py >> gpurun_out/ncu_full_${TAG}.log 2>&1
+$FULL -k regex:wgrad_kernel -s 15 -c 1 -o gpurun_out/prof_wgmx_${TAG} -f python tools/wg_bench.py >> gpurun_out/ncu_full_${TAG}.log 2>&1
+# column-block quantizer, bf16 262144 x 2048: fp32-scale recipe, then MXFP8 (tools/colq_bench.py order)
+$FULL -k regex:quantize_col_tile -s 2 -c 1 -o gpurun_out/prof_colq_${TAG} -f python tools/colq_bench.py >> gpurun_out/ncu_full_${TAG}.log 2>&1
+$FULL -k regex:quantize_col_tile -s 9 -c 1 -o gpurun_out/prof_colqmx_${TAG} -f python tools/colq_bench.py >> gpurun_out/ncu_full_${TAG}.log 2>&1
 echo "profile done"

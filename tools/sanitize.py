@@ -39,6 +39,8 @@ tg.quantize_blocks(torch.randn((2, 256, 384), device=dev))
 xc, xs = tg.quantize_col_blocks(torch.randn((m, 256), device=dev), gs)
 dyc, dys = tg.quantize_col_blocks(torch.randn((m, 128), device=dev), gs)
 tg.wgrad_fp8(xc, xs, dyc, dys, gs)
+dbc, dbs = tg.quantize_col_blocks(torch.randn((m, 128), device=dev), gs, block_cols=128)
+tg.wgrad_fp8(xc, xs, dbc, dbs, gs, dy_block128=True)
 # MXFP8 weight gradient: power-of-two quantizer with factor blocks, block-scaled MMA
 xm, _, xf = tg.quantize_col_blocks_mx(torch.randn((m, 256), device=dev), gs)
 dm, _, df = tg.quantize_col_blocks_mx(torch.randn((m, 256), device=dev), gs)
