@@ -111,6 +111,33 @@ def test_wgrad_matches_oracle(sizes, k, n):
             assert_parity(got[g], want[g], label=f"group {g} (M_g={m})")
 
 
+@pytest.mark.parametrize("sizes,k,n", [
+    ((300, 0, 1, 77, 256), 256, 384),
+    (tuple(range(1, 128, 9)), 128, 256),
+    ((1000, 513), 384, 256),
+])
+def test_wgrad_dy_block128_matches_oracle(sizes, k, n):
+    """TAGG_WGRAD_DY_BLOCK128: dY quantized with one scale per (token block, 128 columns) (the
+    128x128 block recipe, fp8.py:154-176, per group token block); the kernel promotes with
+    s = fl(sx * sdy) once per block and one FFMA2 per pair.  Same oracle, same tolerance."""
+    x, dy = _data(sizes, k, n, 3 * sum(sizes))
+    gs = torch.tensor(sizes, dtype=torch.int32, device=DEV)
+    xc, xs = tg.quantize_col_blocks(torch.from_numpy(x).to(DEV), gs)
+    dc, ds = tg.quantize_col_blocks(torch.from_numpy(dy).to(DEV), gs, block_cols=128)
+    dw = tg.wgrad_fp8(xc, xs, dc, ds, gs, dy_block128=True)
+    torch.cuda.synchronize()
+    tb = sum(-(-s // 128) for s in sizes)
+    dsn = ds[:tb].cpu().numpy()
+    assert np.all(dsn.reshape(tb, n // 128, 128) == dsn.reshape(tb, n // 128, 128)[:, :, :1])
+    want = orc.wgrad(xc.cpu().numpy(), xs[:tb].cpu().numpy(), dc.cpu().numpy(), dsn, sizes, threads=8)
+    got = dw.view(torch.int16).cpu().numpy().view(np.uint16)
+    for g, m in enumerate(sizes):
+        if m == 0:
+            assert np.all(got[g] == 0), "an empty group's gradient is zero"
+        else:
+            assert_parity(got[g], want[g], label=f"group {g} (M_g={m})")
+
+
 def test_wgrad_never_reads_the_next_group():
     """Poison the rows after a short group: its gradient must not change."""
     sizes = (70, 300)
