@@ -24,6 +24,12 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
   return r;
 }
 
+__device__ __forceinline__ uint64_t opaque_u64(uint64_t v) {
+  uint64_t r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(v));
+  return r;
+}
+
 // ---------------------------------------------------------------- mbarrier
 // Bounded spin: a protocol bug traps (error 719) instead of hanging the GPU.
 #ifndef TAGG_WAIT_LIMIT

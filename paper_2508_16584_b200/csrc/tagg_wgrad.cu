@@ -732,8 +732,10 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
   uint32_t live_rows = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) live_rows |= (rl + 16 * j < rows ? 1u : 0u) << j;
-  uint8_t* const code_row = codes + (row0 + rl) * ldc;
-  const int64_t code_step = 16 * ldc;
+  // opaque: kept in registers, not re-derived from the parameters at every store (ptxas
+  // rematerialised the 64-bit products under this kernel's register pressure: +4%)
+  uint8_t* const code_row = reinterpret_cast<uint8_t*>(opaque_u64(reinterpret_cast<uint64_t>(codes + (row0 + rl) * ldc)));
+  const int64_t code_step = static_cast<int64_t>(opaque_u64(static_cast<uint64_t>(16 * ldc)));
   auto value = [&](const ColChunk<kBf16>& ch, int j, int k) -> float {
     const float f = ch.get(j, k);
     return kWeighted ? __fmul_rn(wr[j], f) : f;  // weighted rows are fl(w * x), as gathered
