@@ -3,6 +3,8 @@
 // flight into a ring of shared-memory stages, over a buffer small enough to stay in L2.
 //   mode 0: every CTA walks the same boxes (shared operand tiles, as in a GEMM wave)
 //   mode 1: CTA c starts at box 97 c (mostly distinct boxes at any moment)
+//   mode 2: as 1, over a [rows, 7168 B] matrix: each box row is a 128-B piece of a 7168-B row (the
+//           GEMMs' operand boxes: K-major A rows, token rows of X and dY)
 // Prints TB/s and bytes per SM clock (chip-wide).  Build: see tools/micro/README or
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o l2_tma_bw l2_tma_bw.cu -lcuda
 #include <cuda.h>
@@ -40,12 +42,13 @@ __global__ void __launch_bounds__(32, 1) stream_boxes(const __grid_constant__ CU
     }
     if (i < iters) {
       const int box = (start + i) % nbox;
+      const int bx = mode == 2 ? (box % 56) * 128 : 0, by = mode == 2 ? (box / 56) * 128 : box * 128;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[st])), "r"(kBox)
                    : "memory");
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
               smem_u32(ring + st * kBox)),
-          "l"(&map), "r"(0), "r"(box * 128), "r"(smem_u32(&full[st]))
+          "l"(&map), "r"(bx), "r"(by), "r"(smem_u32(&full[st]))
           : "memory");
     }
   }
@@ -56,14 +59,16 @@ int main(int argc, char** argv) {
   const int mode = argc > 1 ? atoi(argv[1]) : 0;
   const int mb = argc > 2 ? atoi(argv[2]) : 32;  // buffer MB (L2-resident when well under 126)
   const int iters = 4096;
-  const int nbox = (mb << 20) / kBox;
+  int nbox = (mb << 20) / kBox;
+  if (mode == 2) nbox -= nbox % 56;  // whole 7168-B rows
   uint8_t* buf;
   cudaMalloc(&buf, static_cast<size_t>(nbox) * kBox);
   cudaMemset(buf, 1, static_cast<size_t>(nbox) * kBox);
   // the buffer as a [nbox * 128 rows, 128 B] u8 matrix, boxes of 128 x 128 B, 128B swizzle
   CUtensorMap map;
-  const cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(nbox) * 128};
-  const cuuint64_t strides[1] = {128};
+  const cuuint64_t dims[2] = {mode == 2 ? 7168u : 128u,
+                              static_cast<cuuint64_t>(nbox) * 128 / (mode == 2 ? 56 : 1)};
+  const cuuint64_t strides[1] = {mode == 2 ? 7168u : 128u};
   const cuuint32_t box[2] = {128, 128}, es[2] = {1, 1};
   if (cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, buf, dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
