@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
   uint64_t* tempty = tfull + kNumAcc;
   uint64_t* sfull = tempty + kNumAcc;
   uint64_t* sempty = sfull + kScaleRing;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + kScaleRing);
+  uint64_t* cfull = sempty + kScaleRing;  // [2] per column half: the tile's dW staged (4 warps)
+  uint64_t* cempty = cfull + 2;           // [2] the stores have read the staging (warp 3)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -128,6 +130,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     for (int i = 0; i < kScaleRing; ++i) {
       mbar_init(&sfull[i], 1);
       mbar_init(&sempty[i], kPromoWarps);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&cfull[i], kPromoWarps / 2);
+      mbar_init(&cempty[i], 1);
     }
     fence_mbar_init();
   }
@@ -245,8 +251,32 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
       // sx[tb][kr..+128) and sdy[tb][n0..+256) of each token block into the scale ring, on a warp
       // of their own: a bulk-copy issue holds its warp, and on the operand producer's warp the
       // two per block paced the pipeline.
-      uint32_t sring = 0, sph = 0;
+      // It also issues the dW stores: the promotion warps stage a tile and hand it over through
+      // cfull[h], and get the staging back through cempty[h] once the stores have read it (a TMA
+      // store holds its issuing warp, which in a promotion warp delayed its next drain and with
+      // it the MMA chain).  Tile t's stores go out after tile t + 1's scales are requested.
+      uint32_t sring = 0, sph = 0, cph = 0;
       const uint32_t sS0 = smem_u32(smem + p.off_s);
+      const uint32_t cfull0 = smem_u32(&cfull[0]), cempty0 = smem_u32(&cempty[0]);
+      auto store_tile = [&](int t) {
+        const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
+        const int n0 = (rem % p.NT) * 256, kr = (rem / p.NT) * 256 + 128 * rank;
+        mbar_wait_addr(cfull0, cph);
+        mbar_wait_addr(cfull0 + 8, cph);
+        cph ^= 1;
+        if (lane == 0) {
+          if (kr < p.K) {
+            for (int c = 0; c < 4; ++c)
+              if (n0 + 64 * c < p.N) tma_store_2d(&p.map_dw, smem + p.off_c + c * kChunkC, n0 + 64 * c, g * p.K + kr);
+            bulk_commit();
+          }
+          bulk_wait_read0();  // the stores have read the staging
+          mbar_arrive_addr(cempty0);
+          mbar_arrive_addr(cempty0 + 8);
+        }
+        __syncwarp();
+      };
+      int tprev = -1;
       for (int t = cid; t < tiles; t += nclusters) {
         const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
         const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
@@ -266,7 +296,12 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
           __syncwarp();
           if (++sring == kScaleRing) { sring = 0; sph ^= 1; }
         }
+        if (tprev >= 0) store_tile(tprev);
+        tprev = t;
       }
+      if (tprev >= 0) store_tile(tprev);
+      if (lane == 0) bulk_wait0();
+      __syncwarp();
     } else if (kMx && warp == 3) {
       // ====================================================== E8M0 factor loads (kMx, both CTAs)
       // The stage's factor blocks ride on its full barrier (the leader's expect_tx counts them); a
@@ -382,6 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
     uint32_t acc_i = 0, accph = 0, sring = 0, sph = 0, kiter = 0, tiles_done = 0;
     const bool tr = p.trace != nullptr && pw == 0 && lane == 0;
     uint32_t mx_ph = 0;  // kMx: parity of the single accumulator's handoffs
+    uint32_t cph = 0;    // promotion recipes: parity of the staging handoffs with warp 3
+    const uint32_t cfull0 = opaque_u32(smem_u32(&cfull[0])), cempty0 = opaque_u32(smem_u32(&cempty[0]));
     for (int t = cid; t < tiles; t += nclusters) {
       const int g = t / (p.KT * p.NT), rem = t % (p.KT * p.NT);
       const int k0 = (rem / p.NT) * 256, n0 = (rem % p.NT) * 256;
@@ -487,7 +524,24 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
       // 2h+1 (their 128 columns), sync only among themselves (named barrier 2 + h) and their first
       // thread stores them (a TMA store's smem reads are tracked per issuing thread, so each leader
       // waits for its own before the slot is rewritten).
-      {
+      if constexpr (!kMx) {
+        // hand the staged tile to warp 3, which stores it (see there)
+        mbar_wait_addr(cempty0 + 8 * half, cph ^ 1);
+        const uint32_t base = smem_u32(smem + p.off_c) + static_cast<uint32_t>(r) * 128u;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const uint32_t chunk = 2 * half + (jj >> 3);
+          const uint32_t w0 = pack_bf16x2(acc[8 * jj + 0], acc[8 * jj + 1]);
+          const uint32_t w1 = pack_bf16x2(acc[8 * jj + 2], acc[8 * jj + 3]);
+          const uint32_t w2 = pack_bf16x2(acc[8 * jj + 4], acc[8 * jj + 5]);
+          const uint32_t w3 = pack_bf16x2(acc[8 * jj + 6], acc[8 * jj + 7]);
+          st_shared_v4(base + chunk * kChunkC + static_cast<uint32_t>(((jj & 7) ^ (r & 7)) * 16), w0, w1, w2, w3);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_addr(cfull0 + 8 * half);
+        cph ^= 1;
+      } else {
         constexpr int kEpiPasses = epi_passes(kMx);
         constexpr int kCpp = 2 / kEpiPasses;  // chunks per half per pass
         const int hl = 128 * half;
@@ -521,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_kernel(const __grid_constan
       if (tr) wg_stamp(p.trace, kWgEpiEnd, tiles_done);
       ++tiles_done;
     }
-    if (ptid == 0 || ptid == 128) bulk_wait0();  // both column-half leaders issue stores
+    if (kMx && (ptid == 0 || ptid == 128)) bulk_wait0();  // MXFP8: both column-half leaders issue stores
   }
   __syncwarp();
   tc_fence_before();
@@ -1091,7 +1145,7 @@ static int wgrad_launch(const void* x, const float* sx, const void* dy, const fl
   p.off_tab = p.off_sf + kStages * kSfStage;
   const uint32_t tab = static_cast<uint32_t>(((3 * G * 4) + 15) & ~15);
   p.off_bar = p.off_tab + tab;
-  const uint32_t smem = p.off_bar + (2 * kStages + 2 * kNumAcc + 2 * kScaleRing) * 8 + 16 + 1024;
+  const uint32_t smem = p.off_bar + (2 * kStages + 2 * kNumAcc + 2 * kScaleRing + 4) * 8 + 16 + 1024;
   if (smem > 232448) return TAGG_ERR_UNSUPPORTED;
   const bool dy_block = !mx && (flags & TAGG_WGRAD_DY_BLOCK128) != 0;
   const int variant = mx ? 2 : (dy_block ? 1 : 0);
