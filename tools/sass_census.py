@@ -2,7 +2,7 @@
 prove the tcgen05 / TMA path (UTCQMMA = tcgen05.mma kind::f8f6f4, LDTM = tcgen05.ld, UTMALDG /
 UTMASTG = TMA tensor load / store, UBLKCP = 1-D bulk copy), the promotion math (FFMA2, FMUL2),
 the bf16 packs, and every local-memory spill with the source line it is attributed to
-(nvdisasm -g; the build uses -lineinfo).  Writes profiles/sass_census_r02b.json."""
+(nvdisasm -g; the build uses -lineinfo).  Writes profiles/sass_census_r02c.json."""
 import collections
 import json
 import re
@@ -45,7 +45,7 @@ def main():
                         spills.append(f"{op} @ {line}")
                 dem = subprocess.run(["c++filt"], input=name, capture_output=True, text=True).stdout.strip()
                 out[dem] = {"file": cub.name, "ops": dict(ops), "local_memory": spills}
-    dst = ROOT / "profiles" / "sass_census_r02b.json"
+    dst = ROOT / "profiles" / "sass_census_r02c.json"
     dst.write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
     for k, v in out.items():
         if "gemm_kernel" in k or "wgrad" in k:
