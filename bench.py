@@ -1066,8 +1066,21 @@ def run_moe_ffn(torch, tg, dev, fp8_peak, tokens=32768, topk=8, experts=256, hid
     grads = moe.moe_ffn_backward(dy, ctx, w, marks=marks)
     torch.cuda.synchronize()
     breakdown = {marks[i][0]: marks[i - 1][1].elapsed_time(marks[i][1]) for i in range(1, len(marks))}
+    # the same backward with the other weight-gradient recipes (moe_ffn_backward(wgrad_recipe=))
+    recipes = {}
+    for recipe in ("dy_block128", "mxfp8"):
+        moe.moe_ffn_backward(dy, ctx, w, wgrad_recipe=recipe)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(bw_iters):
+            grads = moe.moe_ffn_backward(dy, ctx, w, wgrad_recipe=recipe)
+        e.record()
+        torch.cuda.synchronize()
+        r_ms = s.elapsed_time(e) / bw_iters
+        recipes[recipe] = {"ms": r_ms, "tflops": 2 * flops / (r_ms * 1e-3) / 1e12}
     del grads, ctx
     res["backward"] = {"ms": bw_ms, "tflops": 2 * flops / (bw_ms * 1e-3) / 1e12, "breakdown_ms": breakdown,
+                       "wgrad_recipe": "per_column", "other_wgrad_recipes": recipes,
                        "dw_bytes": 2 * experts * hidden * 3 * inter,
                        "note": "dgrad x2 (b_layout nk), K9, wgrad x2 (K6, column-block quantized operands), "
                                "dx combine (K8), row gathers (K10), router grads (K11)"}

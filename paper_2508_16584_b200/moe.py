@@ -184,17 +184,41 @@ def _mark(marks, name):
         marks.append((name, ev))
 
 
-def moe_ffn_backward(dy: torch.Tensor, ctx: MoeContext, w: ExpertWeights, *, marks: list | None = None) -> MoeGrads:
+WGRAD_RECIPES = ("per_column", "dy_block128", "mxfp8")
+
+
+def moe_ffn_backward(dy: torch.Tensor, ctx: MoeContext, w: ExpertWeights, *, marks: list | None = None,
+                     wgrad_recipe: str = "per_column") -> MoeGrads:
     """Backward of moe_ffn, padding-free end to end.
 
     * dgrad: the two GEMMs again with the same FP8 weights read K-major (b_layout "nk");
     * SwiGLU backward + quantize (K9);
-    * wgrad: the K-grouped GEMM (K6) over column-quantized activations and gradients;
+    * wgrad: the K-grouped GEMM (K6) over column-quantized activations and gradients, in one of
+      three recipes (``wgrad_recipe``): "per_column" fp32 scales per (token block, column) on
+      both sides (the default), "dy_block128" the gradient side with one scale per (token block,
+      128 columns) (one FFMA2 per pair in the promotion), or "mxfp8" power-of-two scales applied
+      by the tensor core (no per-block promotion);
     * dx: the top-k combine (K8) with unit weights; d(router weights): row dot products.
     Row gathers (K10) and the router-weight dot products (K11) are kernels too; only index
     arithmetic on [R] int vectors is torch.
     """
-    from .wgrad import quantize_col_blocks, wgrad_fp8
+    from .wgrad import quantize_col_blocks, quantize_col_blocks_mx, wgrad_fp8, wgrad_fp8_mx
+
+    if wgrad_recipe not in WGRAD_RECIPES:
+        raise InvalidInput(f"wgrad_recipe must be one of {WGRAD_RECIPES}")
+
+    def wgrad(xs, xi, xw, ys, yi, yw, name):
+        """dW = X^T dY per group; X / dY rows optionally gathered (index) and weighted."""
+        if wgrad_recipe == "mxfp8":
+            xq, _, xf = quantize_col_blocks_mx(xs, gs, index=xi, row_weights=xw)
+            yq, _, yf = quantize_col_blocks_mx(ys, gs, index=yi, row_weights=yw)
+            _mark(marks, name + "_quantize")
+            return wgrad_fp8_mx(xq, xf, yq, yf, gs)
+        xq, xsc = quantize_col_blocks(xs, gs, index=xi, row_weights=xw)
+        block = wgrad_recipe == "dy_block128"
+        yq, ysc = quantize_col_blocks(ys, gs, index=yi, row_weights=yw, block_cols=128 if block else 1)
+        _mark(marks, name + "_quantize")
+        return wgrad_fp8(xq, xsc, yq, ysc, gs, dy_block128=block)
 
     _mark(marks, "start")
     d = ctx.dispatch
@@ -218,15 +242,10 @@ def moe_ffn_backward(dy: torch.Tensor, ctx: MoeContext, w: ExpertWeights, *, mar
     dx = combine(dxd, d.dest_rows, torch.ones((t, topk), dtype=torch.float32, device=dy.device))
     _mark(marks, "dx_combine")
     # wgrad: dW_down = H2^T dC, dW_gu = X^T dGU, per group
-    hq, hs = quantize_col_blocks(ctx.v, gs)
-    cq, cs = quantize_col_blocks(dy, gs, index=src, row_weights=w_rows)  # w[t,k] dy[t], gathered in place
-    _mark(marks, "wgrad_down_quantize")
-    dw_down = wgrad_fp8(hq, hs, cq, cs, gs)
+    # (dC rows are w[t,k] dy[t] and X rows x[t], both gathered in place by the quantizer)
+    dw_down = wgrad(ctx.v, None, None, dy, src, w_rows, "wgrad_down")
     _mark(marks, "wgrad_down")
-    xq, xsc = quantize_col_blocks(ctx.x, gs, index=src)                # x[t], gathered in place
-    gq, gsc = quantize_col_blocks(dgu, gs)
-    _mark(marks, "wgrad_gate_up_quantize")
-    dw_gate_up = wgrad_fp8(xq, xsc, gq, gsc, gs)
+    dw_gate_up = wgrad(ctx.x, src, None, dgu, None, None, "wgrad_gate_up")
     _mark(marks, "wgrad_gate_up")
     # d(router weight)[t, k] = <dy[t], c[dest(t, k)]>
     dweights = router_grad(dy, ctx.c, d.dest_rows, topk)

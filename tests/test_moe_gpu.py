@@ -111,7 +111,8 @@ def _dequant_blocks(codes, scales):
     return v * s
 
 
-def test_moe_ffn_backward_matches_float64():
+@pytest.mark.parametrize("recipe", ["per_column", "dy_block128", "mxfp8"])
+def test_moe_ffn_backward_matches_float64(recipe):
     """moe_ffn(save=True) + moe_ffn_backward against float64 math on the same (dequantized) FP8
     weights.  Activations and gradients pass through 1x128 / column-block FP8 on the GPU, so
     each gradient is compared by relative Frobenius error."""
@@ -128,7 +129,7 @@ def test_moe_ffn_backward_matches_float64():
     weights = moe.ExpertWeights(c1, s1, c2, s2)
     xb = torch.from_numpy(x).to(DEV).to(torch.bfloat16)
     y, ctx = moe.moe_ffn(xb, torch.from_numpy(eids).to(DEV), torch.from_numpy(wts).to(DEV), weights, save=True)
-    g = moe.moe_ffn_backward(torch.from_numpy(dy).to(DEV).to(torch.bfloat16), ctx, weights)
+    g = moe.moe_ffn_backward(torch.from_numpy(dy).to(DEV).to(torch.bfloat16), ctx, weights, wgrad_recipe=recipe)
     torch.cuda.synchronize()
     W1 = _dequant_blocks(c1.cpu().numpy(), s1.cpu().numpy())
     W2 = _dequant_blocks(c2.cpu().numpy(), s2.cpu().numpy())
