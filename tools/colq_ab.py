@@ -1,5 +1,6 @@
 """A/B timing of libtagg builds' column-block quantizer (bf16, 262144 grouped rows, 256 groups):
-python tools/colq_ab.py A.so B.so ...  (ABBA rounds; GB/s counts one read of x + the codes)."""
+python tools/colq_ab.py [--gather] A.so B.so ...  (ABBA rounds; GB/s counts one read of x + the codes;
+--gather: the weighted gather form from a token-ordered tensor)."""
 import ctypes
 import sys
 
@@ -8,7 +9,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2508_16584_b200 import _lib  # noqa: E402
 
-libs = sys.argv[1:]
+GATHER = "--gather" in sys.argv
+libs = [a for a in sys.argv[1:] if a != "--gather"]
 L = []
 for path in libs:
     lib = ctypes.CDLL(path)
@@ -25,9 +27,20 @@ for cols in (2048, 7168):
     sc = torch.empty((2048 + 256, cols), dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream().cuda_stream
 
+    # gather mode (MoE backward's dC): row r = w[r] * x_tok[index[r]] from a token-ordered
+    # [32768, cols] tensor, top-8 rows per token
+    xt = x[:32768]
+    idx = torch.randint(0, 32768, (262144,), device=dev, dtype=torch.int32)
+    wts = torch.rand(262144, device=dev)
+
     def run(lib):
-        rc = lib.tagg_quantize_col_blocks(x.data_ptr(), 0, 262144, cols, cols, gs.data_ptr(), 256, codes.data_ptr(),
-                                          cols, sc.data_ptr(), err.data_ptr(), st)
+        if GATHER:
+            rc = lib.tagg_quantize_col_blocks_gather(xt.data_ptr(), 0, cols, idx.data_ptr(), wts.data_ptr(), 262144,
+                                                     cols, gs.data_ptr(), 256, codes.data_ptr(), cols, sc.data_ptr(),
+                                                     err.data_ptr(), st)
+        else:
+            rc = lib.tagg_quantize_col_blocks(x.data_ptr(), 0, 262144, cols, cols, gs.data_ptr(), 256,
+                                              codes.data_ptr(), cols, sc.data_ptr(), err.data_ptr(), st)
         assert rc == 0, rc
     times = {p: [] for p in libs}
     for rnd in range(6):
