@@ -798,8 +798,10 @@ __global__ void __launch_bounds__(256, 2) quantize_col_tile_kernel(const void* _
   uint32_t bad = 0;
   // bf16: the next chunk's loads are in flight while this one is reduced and quantized (two
   // 32-register chunks); f32 chunks take 64 registers each, so f32 loads one at a time
-  // (measured: without the prefetch, 3 CTAs per SM run 3-5% slower)
-  constexpr bool kPrefetch = kBf16;
+  // (measured: without the prefetch, 3 CTAs per SM run 3-5% slower).  The weighted gather (the
+  // MoE backward's dC rows) loads one at a time too: with the prefetch it spilled 112 B, and
+  // without it runs 8-10% faster (tools/colq_ab.py --gather).
+  constexpr bool kPrefetch = kBf16 && !kWeighted;
   ColChunk<kBf16> cur;
   if (kPrefetch) cur.load(xrow, min(cg * 8, cols - 8));
   for (int cb = 0; cb < nchunks; ++cb) {
