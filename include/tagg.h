@@ -192,6 +192,14 @@ int tagg_route_error(const int32_t* workspace, int64_t rows, int num_experts, in
 int tagg_quantize_dispatch(const void* x, int x_dtype, int64_t ldx, int64_t tokens, int K, int topk,
                            const int32_t* dest_rows, void* a, int64_t lda, float* sa, int32_t* err_flag,
                            void* stream);
+/*
+ * The same 1x128 quantization over gathered, weighted rows, without materialising them: row r of
+ * a / sa quantizes bf16(row_weights[r] * x[index[r]]) (fl(w*x) rounded to bf16 RNE, i.e. exactly
+ * the rows tagg_gather_scale_rows writes; row_weights may be NULL for a plain gather).  The MoE
+ * backward's dL/dc rows go straight from the token-ordered dy to the dgrad GEMM's A / S_A.
+ */
+int tagg_quantize_gather_rows(const void* x, int x_dtype, int64_t ldx, const int32_t* index, const float* row_weights,
+                              int64_t rows, int K, void* a, int64_t lda, float* sa, int32_t* err_flag, void* stream);
 
 /*
  * 128x128 block quantization (fp8.py:154-176), batched: matrix b of x (rows x cols,

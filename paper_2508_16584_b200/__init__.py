@@ -41,6 +41,7 @@ from .quant import (  # noqa: F401
     gather_rows,
     quantize_blocks,
     quantize_dispatch,
+    quantize_gather_rows,
     quantize_row_tiles,
     route_plan,
 )

@@ -56,6 +56,7 @@ SIGNATURES = {
                                               c_i64, c_vp, c_vp, c_vp]),
     "tagg_route_plan": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_vp]),
     "tagg_route_error": (c_int, [c_vp, c_i64, c_int, c_vp]),
+    "tagg_quantize_gather_rows": (c_int, [c_vp, c_int, c_i64, c_vp, c_vp, c_i64, c_int, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "tagg_quantize_dispatch": (c_int, [c_vp, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_i64, c_vp, c_vp,
                                        c_vp]),
     "tagg_validate_config": (c_int, [c_i64, c_i64, c_vp, c_int, c_i64, c_i64, c_i64]),

@@ -159,10 +159,15 @@ __global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __re
                                                                 int K, int topk, const int32_t* __restrict__ dest,
                                                                 uint8_t* __restrict__ a, int64_t lda,
                                                                 float* __restrict__ sa, int32_t* __restrict__ err,
-                                                                bool vec) {
+                                                                bool vec, const int32_t* __restrict__ gidx = nullptr,
+                                                                const float* __restrict__ gw = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= T) return;
+  // gather form (Q5): row t quantizes bf16(gw[t] * x[gidx[t]]) -- K10's rows, never written out
+  const int64_t xr = gidx ? static_cast<int64_t>(gidx[t]) : t;
+  const float wrow = (gidx && gw) ? gw[t] : 1.0f;
+  const bool scaled = gidx != nullptr && gw != nullptr;
   const int kb = (K + 127) / 128;
   int32_t d[8];
 #pragma unroll
@@ -178,8 +183,8 @@ __global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __re
   auto full_at = [&](int tile0) { return vec && (tile0 + sub) * 128 + 16 * part + 15 < K; };
   auto load_raw = [&](int tile0, uint4 (&r)[kRaw]) {
     const int c0 = (tile0 + sub) * 128 + 16 * part;
-    const uint4* src = kBf16 ? reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + t * ldx + c0)
-                             : reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(x) + t * ldx + c0);
+    const uint4* src = kBf16 ? reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + xr * ldx + c0)
+                             : reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(x) + xr * ldx + c0);
 #pragma unroll
     for (int j = 0; j < kRaw; ++j) r[j] = __ldcs(src + j);  // read once: stream past L2
   };
@@ -219,10 +224,20 @@ __global__ void __launch_bounds__(256) quantize_dispatch_kernel(const void* __re
         v[j] = 0.0f;
         if (tile < kb && c0 + j < K) {
           if constexpr (kBf16)
-            v[j] = __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(x)[t * ldx + c0 + j]) << 16);
+            v[j] = __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(x)[xr * ldx + c0 + j]) << 16);
           else
-            v[j] = reinterpret_cast<const float*>(x)[t * ldx + c0 + j];
+            v[j] = reinterpret_cast<const float*>(x)[xr * ldx + c0 + j];
         }
+      }
+    }
+    if (scaled) {
+      // K10's value: bf16(fl(w * x)), round to nearest even (cvt.rn.bf16x2)
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        uint32_t pr;
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pr) : "f"(__fmul_rn(wrow, v[j + 1])), "f"(__fmul_rn(wrow, v[j])));
+        v[j] = __uint_as_float(pr << 16);
+        v[j + 1] = __uint_as_float(pr & 0xFFFF0000u);
       }
     }
     float amax = 0.0f;
@@ -382,6 +397,30 @@ extern "C" int tagg_route_error(const int32_t* workspace, int64_t rows, int num_
                  cudaSuccess
              ? TAGG_OK
              : TAGG_ERR_CUDA;
+}
+
+extern "C" int tagg_quantize_gather_rows(const void* x, int x_dtype, int64_t ldx, const int32_t* index,
+                                         const float* row_weights, int64_t rows, int K, void* a, int64_t lda,
+                                         float* sa, int32_t* err_flag, void* stream) {
+  if (K < 1 || rows < 0) return TAGG_ERR_CONFIG;
+  if (x_dtype != TAGG_DTYPE_BF16 && x_dtype != TAGG_DTYPE_F32) return TAGG_ERR_CONFIG;
+  if (ldx < K || lda < K) return TAGG_ERR_SHAPE;
+  if (rows == 0) return TAGG_OK;
+  if (!x || !index || !a || !sa || !err_flag) return TAGG_ERR_SHAPE;
+  const int esz = x_dtype == TAGG_DTYPE_BF16 ? 2 : 4;
+  const bool vec = !(reinterpret_cast<uintptr_t>(x) % 16) && !((ldx * esz) % 16) &&
+                   !(reinterpret_cast<uintptr_t>(a) % 16) && !(lda % 16);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int warps = 8;
+  const int64_t blocks = (rows + warps - 1) / warps;
+  if (blocks >= (int64_t(1) << 31)) return TAGG_ERR_UNSUPPORTED;
+  if (x_dtype == TAGG_DTYPE_BF16)
+    quantize_dispatch_kernel<true><<<static_cast<unsigned>(blocks), 32 * warps, 0, st>>>(
+        x, ldx, rows, K, 1, nullptr, static_cast<uint8_t*>(a), lda, sa, err_flag, vec, index, row_weights);
+  else
+    quantize_dispatch_kernel<false><<<static_cast<unsigned>(blocks), 32 * warps, 0, st>>>(
+        x, ldx, rows, K, 1, nullptr, static_cast<uint8_t*>(a), lda, sa, err_flag, vec, index, row_weights);
+  return cudaGetLastError() == cudaSuccess ? TAGG_OK : TAGG_ERR_CUDA;
 }
 
 extern "C" int tagg_quantize_dispatch(const void* x, int x_dtype, int64_t ldx, int64_t tokens, int K, int topk,

@@ -229,9 +229,8 @@ def moe_ffn_backward(dy: torch.Tensor, ctx: MoeContext, w: ExpertWeights, *, mar
     order[dest] = torch.arange(dest.numel(), device=dest.device)   # grouped row -> (token, k)
     src = order // topk
     w_rows = ctx.weights.reshape(-1).index_select(0, order).to(torch.float32)
-    # dL/dc for the grouped rows: w[t,k] * dy[t] (K10), then 1x128 rows for the dgrad GEMM
-    dc = gather_scale_rows(dy, src, w_rows)
-    dc_codes, dc_scales = quant.quantize_row_tiles(dc)
+    # dL/dc for the grouped rows: w[t,k] * dy[t] (K10's values), 1x128-quantized in the same pass
+    dc_codes, dc_scales = quant.quantize_gather_rows(dy, src, w_rows)  # K10's rows, quantized in place
     _mark(marks, "dc_gather_quantize")
     dh2 = grouped_gemm_fp8(dc_codes, dc_scales, w.w_down, w.s_down, gs, b_layout="nk")
     _mark(marks, "dgrad_down")

@@ -93,6 +93,34 @@ def quantize_row_tiles(x: torch.Tensor, *, check: bool = False):
     return _quantize(x, 1, None, x.shape[0], check)
 
 
+def quantize_gather_rows(x: torch.Tensor, index: torch.Tensor, row_weights: torch.Tensor | None = None, *,
+                         check: bool = False):
+    """quantize_row_tiles(bf16(row_weights[r] * x[index[r]])) without materialising the gathered rows
+    (tagg_quantize_gather_rows): the codes and scales are bit-identical to gathering with
+    moe.gather_scale_rows (K10) and then quantizing.  x: [T, K] bf16 / f32; index: int [R]."""
+    _check_cuda(x, "x")
+    if x.dim() != 2 or x.dtype not in _DTYPES or x.stride(1) != 1:
+        raise ShapeMismatch("x must be a row-major bf16 / f32 matrix")
+    idx = index.to(torch.int32).contiguous()
+    w = None if row_weights is None else row_weights.to(torch.float32).contiguous()
+    r, k = idx.numel(), x.shape[1]
+    if k < 1:
+        raise InvalidInput("matrix must have at least one column")
+    kb = -(-k // 128)
+    lda = -(-k // 16) * 16
+    a = torch.empty((r, lda), dtype=torch.uint8, device=x.device)
+    sa = torch.empty((r, kb), dtype=torch.float32, device=x.device)
+    err = torch.zeros(1, dtype=torch.int32, device=x.device)
+    if r:
+        rc = lib().tagg_quantize_gather_rows(x.data_ptr(), _DTYPES[x.dtype], x.stride(0), idx.data_ptr(),
+                                             None if w is None else w.data_ptr(), r, k, a.data_ptr(), lda,
+                                             sa.data_ptr(), err.data_ptr(), _stream())
+        raise_for_status(rc, "tagg_quantize_gather_rows")
+    if check and int(err.item()):
+        raise InvalidInput("matrix entries must be finite")
+    return a[:, :k], sa
+
+
 def quantize_blocks(w: torch.Tensor, *, check: bool = False):
     """fp8.py:154-176 on the GPU, batched over leading dims: one scale per 128x128 block.
 

@@ -111,6 +111,24 @@ def _dequant_blocks(codes, scales):
     return v * s
 
 
+@pytest.mark.parametrize("k", [7168, 200, 128])
+@pytest.mark.parametrize("weighted", [True, False])
+def test_quantize_gather_rows_equals_gather_then_quantize(k, weighted):
+    """tagg_quantize_gather_rows (row r = bf16(w[r] * x[index[r]]), quantized in one pass) is
+    bit-identical to K10's gathered rows quantized by quantize_row_tiles."""
+    torch.manual_seed(k)
+    t, r = 300, 1000
+    x = (torch.randn((t, k), device=DEV) * 4).to(torch.bfloat16)
+    idx = torch.randint(0, t, (r,), device=DEV, dtype=torch.int32)
+    w = torch.rand(r, device=DEV) * 2 if weighted else None
+    got_c, got_s = tg.quantize_gather_rows(x, idx, w, check=True)
+    dc = moe.gather_scale_rows(x, idx, w)
+    want_c, want_s = tg.quantize_row_tiles(dc)
+    torch.cuda.synchronize()
+    assert torch.equal(got_c, want_c)
+    assert torch.equal(got_s.view(torch.int32), want_s.view(torch.int32))
+
+
 @pytest.mark.parametrize("recipe", ["per_column", "dy_block128", "mxfp8"])
 def test_moe_ffn_backward_matches_float64(recipe):
     """moe_ffn(save=True) + moe_ffn_backward against float64 math on the same (dequantized) FP8
